@@ -1,0 +1,212 @@
+/*
+ * critprob_b200.h -- C ABI of the B200-native critical-point probability path.
+ *
+ * Drop-in boundary for the grid hot path of the reference package
+ * `critprob` (arXiv 2407.18015).  The reference has no FFI: its boundary is
+ * the Python API, and each entry point below replaces one step of it
+ * (citations are /root/reference/pkg/src/critprob/<file>:<line>):
+ *
+ *   cpb_fit              UncertainField.from_ensemble      fields.py:125-158
+ *   cpb_from_scalar      UncertainField.from_scalar        fields.py:160-178
+ *   cpb_epsilon          default_epsilon                   distributions.py:30-36
+ *   cpb_classify_closed  classify_field, closed form       engine.py:716-787 (+ _closed_chunk 594-629)
+ *   cpb_classify_mc      classify_field, monte_carlo       engine.py:716-787 (+ _mc_chunk 659-666)
+ *   cpb_materialize      UncertainField.params             fields.py:86-103 (reference f64 layout)
+ *   cpb_unit_block       rngstream.unit_block              rngstream.py:33-48
+ *   cpb_run_host         from_ensemble + classify_field with host buffers (one call, H2D/D2H inside)
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no framework types.  "d_" pointers are CUDA
+ *     device memory, "h_" pointers host memory.  `stream` is a cudaStream_t
+ *     (NULL = legacy default stream).  Calls only enqueue work unless noted.
+ *   - Every function returns a cpb_status; cpb_last_error() describes the
+ *     last failure on the calling thread.
+ *   - The library never frees caller memory.  A cpb_field only carries
+ *     pointers to caller-owned device planes (see cpb_field_plane_bytes).
+ *   - Grids are row-major (H, W); ensembles are member-major (M, H, W)
+ *     float32, exactly the reference's EnsembleStack layout (fields.py:42-56).
+ *   - Results are identical for any launch configuration or row-slab split
+ *     (the reference's worker-count invariance, engine.py:724-727).
+ */
+#ifndef CRITPROB_B200_H
+#define CRITPROB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CPB_ABI_VERSION 1
+
+typedef enum {
+  CPB_OK = 0,
+  CPB_EINVAL = 1,      /* invalid argument (reference: ValueError) */
+  CPB_ECUDA = 2,       /* CUDA runtime error */
+  CPB_ENOMEM = 4,      /* device or pinned-host allocation failed */
+  CPB_ENONFINITE = 5   /* ensemble holds NaN/Inf (reference: ValueError, fields.py:54-55) */
+} cpb_status;
+
+/* Model kinds (fields.py:21, MODEL_KINDS order). */
+enum { CPB_UNIFORM = 0, CPB_EPANECHNIKOV = 1, CPB_HISTOGRAM = 2, CPB_GAUSSIAN = 3 };
+
+/* Channel bits (fields.py:22, CHANNELS). */
+enum { CPB_CH_MIN = 1, CPB_CH_MAX = 2, CPB_CH_SADDLE = 4, CPB_CH_ALL = 7 };
+
+/* Monte Carlo uniform streams. */
+enum {
+  CPB_RNG_SPLITMIX = 0, /* the reference keyed splitmix64 stream: bit-exact (rngstream.py) */
+  CPB_RNG_PHILOX = 1    /* Philox4x32-10 keyed by (seed, pixel, plane): statistical parity only */
+};
+
+/* Storage of the support bounds / histogram weights inside a cpb_field. */
+enum {
+  CPB_BOUNDS_F32_FITTED = 0, /* lo/hi = raw member min/max (exact in f32); lo==hi pixels are
+                                widened by eps/2 at use, as fields.py:140-143 does at fit time */
+  CPB_BOUNDS_F64 = 1         /* lo/hi given in float64 and used as-is (user-built fields) */
+};
+enum {
+  CPB_WEIGHTS_U8 = 0,  /* member counts per bin (members <= 255); weight = count / members */
+  CPB_WEIGHTS_U16 = 1, /* member counts per bin (members <= 65535) */
+  CPB_WEIGHTS_F64 = 2  /* float64 weights as given (user-built fields) */
+};
+
+/*
+ * Compact device-resident fitted field (a row slab of the global grid).
+ * Planes are row-major (height, width); histogram weights are bin planes
+ * (bins, height, width) so every per-bin read is coalesced.
+ *
+ *   uniform / histogram : lo, hi  (float if bounds == F32_FITTED else double)
+ *   epanechnikov        : mean, spread (spread = std(ddof=1) when fitted; the
+ *                         half-width used is max(k * spread, eps / 2), i.e.
+ *                         fields.py:156.  User-built fields pass k = 1, eps = 0
+ *                         and spread = half-width.)
+ *   gaussian            : mean, spread (= stddev)
+ *   histogram           : weights (CPB_WEIGHTS_*), weight_table = d_ptr to
+ *                         (members + 1) doubles c / members (filled by cpb_fit)
+ */
+typedef struct cpb_field {
+  int32_t kind;
+  int32_t bins;
+  int32_t members;
+  int32_t bounds;        /* CPB_BOUNDS_* */
+  int32_t weights_mode;  /* CPB_WEIGHTS_* */
+  int32_t reserved;
+  int64_t height;        /* local rows (a slab includes its halo rows) */
+  int64_t width;
+  int64_t row0;          /* global row index of local row 0 (Monte Carlo pixel keys) */
+  int64_t global_width;  /* pixel key = global_row * global_width + col (engine.py:752-754) */
+  double eps;            /* from the GLOBAL ensemble range (distributions.py:30-36) */
+  double k;              /* epanechnikov k (fields.py:31) */
+  void* lo;
+  void* hi;
+  double* mean;
+  double* spread;
+  void* weights;
+  double* weight_table;
+} cpb_field;
+
+/* ABI version and last error (thread-local). */
+int cpb_abi_version(void);
+const char* cpb_last_error(void);
+
+/* Bytes of device memory each plane of a fitted field needs
+ * (lo, hi, mean, spread, weights, weight_table, range scratch), written into
+ * out[7].  Mirrors the layout cpb_fit writes. */
+int cpb_field_plane_bytes(int32_t kind, int32_t bins, int32_t members, int64_t height,
+                          int64_t width, size_t out[7]);
+
+/* eps = max(1e-12, 1e-9 * (gmax - gmin))  -- distributions.py:30-36. */
+double cpb_epsilon(double gmin, double gmax);
+
+/*
+ * Fit one model per pixel over the member axis (fields.py:133-158).
+ * d_ens: member-major float32, element (m, r, c) at d_ens[m * member_stride + r * width + c]
+ *        for local rows r in [0, f->height).
+ * Writes the compact planes of `f` and, into d_range[0..2], the float32 min
+ * and max over all values read plus a non-finite flag (d_range is 3 x
+ * uint32 device words; decode with cpb_read_range; accumulate != 0 merges into
+ * the words instead of resetting them first, for chunked fits).  `f` must have kind, bins,
+ * members, height, width and the plane pointers set; `f->bounds` and
+ * `f->weights_mode` are set by this call.  Bit-exact with the reference:
+ * min/max and counts exactly, mean/std by the same sequential two-pass order.
+ */
+int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
+            int32_t accumulate, void* stream);
+
+/* Synchronously read back a d_range written by cpb_fit; returns
+ * CPB_ENONFINITE if any value was NaN/Inf. */
+int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* stream);
+
+/* Uniform field from a float64 raster with a +-error_bound/2 band
+ * (fields.py:160-178).  d_lo/d_hi are float64 planes; eps is the raster's
+ * epsilon, used when error_bound == 0. */
+int cpb_from_scalar(const double* d_values, int64_t height, int64_t width, double error_bound,
+                    double eps, double* d_lo, double* d_hi, void* stream);
+
+/*
+ * Closed-form min/max/saddle probabilities (engine.py:594-629) for local rows
+ * [row_begin, row_end) and columns [1, width-1); rows row_begin-1 and row_end
+ * must exist in `f`.  Output planes are (f->height, f->width) float64; a NULL
+ * pointer skips that channel.  Entries outside the computed window are not
+ * touched (callers zero them: ProbabilityField.empty, fields.py:209-212).
+ * Gauss-Legendre quadrature on the breakpoint partition in float64.
+ */
+int cpb_classify_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
+                        double* d_pmax, double* d_psaddle, void* stream);
+
+/*
+ * Monte Carlo pattern fractions (engine.py:195-222, 632-666): n_samples joint
+ * inverse-CDF draws per vertex, strict comparisons, p = count / n.  With
+ * CPB_RNG_SPLITMIX the draws are the reference's keyed stream, so counts
+ * are identical to the reference's.  d_counts (optional, int64 x 3 planes
+ * min/max/saddle, same shape as the outputs) receives the raw hit counts.
+ */
+int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,
+                    int64_t n_samples, int32_t rng, double* d_pmin, double* d_pmax,
+                    double* d_psaddle, int64_t* d_counts, void* stream);
+
+/*
+ * Reference-layout float64 parameters (fields.py:86-103, what from_ensemble
+ * returns): uniform/histogram -> d_a = lo, d_b = hi (widened),
+ * d_weights = (H, W, bins) weights; epanechnikov -> d_a = mean,
+ * d_b = halfwidth; gaussian -> d_a = mean, d_b = stddev.
+ */
+int cpb_materialize(const cpb_field* f, double* d_a, double* d_b, double* d_weights,
+                    void* stream);
+
+/* Uniform [0, 1) draws of the keyed splitmix64 stream, shape (npix, planes, n),
+ * samples [start, start + n) -- rngstream.py:33-48. */
+int cpb_unit_block(uint64_t seed, const uint64_t* d_pixels, int64_t npix, int32_t planes,
+                   int64_t start, int64_t n, double* d_out, void* stream);
+
+/* Synthetic member-major ensemble rows [row0, row0 + nrows) of a height x width
+ * grid: value = f32(bowl(r, c) + noise_amp * (2u - 1)), u = keyed stream
+ * (seed, r * width + c, plane m, sample 0).  The host twin is
+ * oracle.critprob_oracle.synthetic_rows (bit-identical). */
+int cpb_synth_ensemble(float* d_ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
+                       int64_t height, double noise_amp, uint64_t seed, void* stream);
+
+/*
+ * One-call host path: host ensemble in, host probabilities out.  Streams the
+ * ensemble through the device in row chunks (H2D overlapped with the fit),
+ * fits, classifies all interior rows and copies the three float64 planes and
+ * the validity mask back.  h_ens should be pinned (cpb_host_alloc) for full
+ * PCIe bandwidth.  method: 0 = closed form, 1 = Monte Carlo.
+ * Synchronous; returns CPB_ENONFINITE on NaN/Inf input.
+ */
+int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t width,
+                 int32_t kind, int32_t bins, double k, int32_t method, uint64_t seed,
+                 int64_t n_samples, uint32_t channels, double* h_pmin, double* h_pmax,
+                 double* h_psaddle, uint8_t* h_valid);
+
+/* Pinned host memory for cpb_run_host buffers. */
+int cpb_host_alloc(void** ptr, size_t bytes);
+int cpb_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CRITPROB_B200_H */

@@ -1,0 +1,35 @@
+"""B200-native critical-point probabilities for uncertain 2-D ensembles (arXiv 2407.18015).
+
+Drop-in for the grid hot path of the reference ``critprob`` package: the
+noise-model fit (``UncertainField.from_ensemble`` / ``from_scalar``), the
+closed-form min/max/saddle stencil and the Monte Carlo estimator
+(``classify_field``), computed by hand-written sm_100a CUDA kernels behind
+the C ABI in include/critprob_b200.h.  There is no CPU fallback.
+"""
+
+from .engine import (
+    COMBINATORIAL_MAX_BINS,
+    ESTIMATOR_METHODS,
+    PATTERNS,
+    EstimatorSpec,
+    classify_field,
+    pixel_index,
+)
+from .fields import (
+    CHANNELS,
+    MODEL_KINDS,
+    EnsembleStack,
+    ModelSpec,
+    ProbabilityField,
+    UncertainField,
+    set_device,
+)
+from .rngstream import unit_block, unit_planes
+from .synth import synthetic_ensemble, synthetic_rows
+
+__all__ = [
+    "CHANNELS", "COMBINATORIAL_MAX_BINS", "ESTIMATOR_METHODS", "MODEL_KINDS", "PATTERNS",
+    "EnsembleStack", "EstimatorSpec", "ModelSpec", "ProbabilityField", "UncertainField",
+    "classify_field", "pixel_index", "set_device", "synthetic_ensemble", "synthetic_rows",
+    "unit_block", "unit_planes",
+]

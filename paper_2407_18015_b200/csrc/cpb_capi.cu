@@ -1,0 +1,370 @@
+// C ABI entry points (include/critprob_b200.h): argument validation, error
+// reporting and the one-call host pipeline.  Kernels live in cpb_fit.cu,
+// cpb_closed.cu and cpb_mc.cu.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "cpb_common.cuh"
+
+namespace cpb {
+
+int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range, bool accumulate,
+               cudaStream_t st);
+int launch_from_scalar(const double* v, int64_t n, double half, double* lo, double* hi,
+                       cudaStream_t st);
+int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cudaStream_t st);
+int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
+                 int64_t height, double amp, uint64_t seed, cudaStream_t st);
+int launch_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, double* pmin,
+                  double* pmax, double* psad, cudaStream_t st);
+int launch_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t n,
+              int rng, double* pmin, double* pmax, double* psad, int64_t* counts, cudaStream_t st);
+int launch_unit_block(uint64_t seed, const uint64_t* px, int64_t npix, int planes, int64_t start,
+                      int64_t n, double* out, cudaStream_t st);
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+  return e == cudaErrorMemoryAllocation ? CPB_ENOMEM : CPB_ECUDA;
+}
+
+static int check_field(const cpb_field* f, bool need_eps) {
+  if (!f) { set_error("field is NULL"); return CPB_EINVAL; }
+  if (f->kind < CPB_UNIFORM || f->kind > CPB_GAUSSIAN) {
+    set_error("unknown model kind %d", f->kind);
+    return CPB_EINVAL;
+  }
+  if (f->height < 0 || f->width < 0) { set_error("negative field extent"); return CPB_EINVAL; }
+  if (f->kind == CPB_HISTOGRAM && f->bins < 1) { set_error("bins must be at least 1"); return CPB_EINVAL; }
+  if (need_eps && !(f->eps >= 0.0)) { set_error("field eps is not set"); return CPB_EINVAL; }
+  return CPB_OK;
+}
+
+}  // namespace cpb
+
+using namespace cpb;
+
+extern "C" {
+
+int cpb_abi_version(void) { return CPB_ABI_VERSION; }
+
+const char* cpb_last_error(void) { return g_err; }
+
+double cpb_epsilon(double gmin, double gmax) {
+  // distributions.py:30-36
+  const double spread = gmax - gmin;
+  const double e = 1e-9 * spread;
+  return e > 1e-12 ? e : 1e-12;
+}
+
+int cpb_field_plane_bytes(int32_t kind, int32_t bins, int32_t members, int64_t height,
+                          int64_t width, size_t out[7]) {
+  if (!out || height < 0 || width < 0 || members < 1) {
+    set_error("invalid field extent");
+    return CPB_EINVAL;
+  }
+  const size_t n = (size_t)height * (size_t)width;
+  for (int i = 0; i < 7; ++i) out[i] = 0;
+  if (kind == CPB_UNIFORM || kind == CPB_HISTOGRAM) {
+    out[0] = out[1] = n * sizeof(float);
+  } else if (kind == CPB_EPANECHNIKOV || kind == CPB_GAUSSIAN) {
+    out[2] = out[3] = n * sizeof(double);
+  } else {
+    set_error("unknown model kind %d", kind);
+    return CPB_EINVAL;
+  }
+  if (kind == CPB_HISTOGRAM) {
+    if (bins < 1) { set_error("bins must be at least 1"); return CPB_EINVAL; }
+    if (members > 65535) { set_error("histogram fit supports at most 65535 members"); return CPB_EINVAL; }
+    out[4] = n * (size_t)bins * (members <= 255 ? 1 : 2);
+    out[5] = (size_t)(members + 1) * sizeof(double);
+  }
+  out[6] = 3 * sizeof(uint32_t);
+  return CPB_OK;
+}
+
+int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
+            int32_t accumulate, void* stream) {
+  int s = check_field(f, false);
+  if (s) return s;
+  if (f->members < 1) { set_error("ensemble needs at least one member"); return CPB_EINVAL; }
+  if (f->members < 2 && (f->kind == CPB_EPANECHNIKOV || f->kind == CPB_GAUSSIAN)) {
+    set_error("%s fit needs at least two members",
+              f->kind == CPB_EPANECHNIKOV ? "epanechnikov" : "gaussian");
+    return CPB_EINVAL;
+  }
+  if (f->kind == CPB_HISTOGRAM && f->members > 65535) {
+    set_error("histogram fit supports at most 65535 members");
+    return CPB_EINVAL;
+  }
+  if (member_stride < f->height * f->width) { set_error("member_stride smaller than a member plane"); return CPB_EINVAL; }
+  if (!d_ens || !d_range) { set_error("NULL ensemble or range pointer"); return CPB_EINVAL; }
+  return launch_fit(d_ens, member_stride, f, d_range, accumulate != 0, (cudaStream_t)stream);
+}
+
+int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* stream) {
+  uint32_t h[3];
+  cudaError_t e = cudaMemcpyAsync(h, d_range, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "read range");
+  if (h[2]) { set_error("ensemble values must be finite"); return CPB_ENONFINITE; }
+  if (gmin) *gmin = (double)ordered_to_float(h[0]);
+  if (gmax) *gmax = (double)ordered_to_float(h[1]);
+  return CPB_OK;
+}
+
+int cpb_from_scalar(const double* d_values, int64_t height, int64_t width, double error_bound,
+                    double eps, double* d_lo, double* d_hi, void* stream) {
+  if (!(error_bound >= 0.0)) { set_error("error bound must be nonnegative"); return CPB_EINVAL; }
+  double half = 0.5 * error_bound;
+  if (half <= 0.0) half = 0.5 * eps;  // fields.py:174-176
+  return launch_from_scalar(d_values, height * width, half, d_lo, d_hi, (cudaStream_t)stream);
+}
+
+int cpb_classify_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
+                        double* d_pmax, double* d_psaddle, void* stream) {
+  int s = check_field(f, true);
+  if (s) return s;
+  if (f->kind == CPB_GAUSSIAN) {
+    set_error("Gaussian fields have no closed form; use monte_carlo");
+    return CPB_EINVAL;
+  }
+  if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
+    if (row_end > row_begin) {
+      set_error("rows [%lld, %lld) need a one-row halo inside the field",
+                (long long)row_begin, (long long)row_end);
+      return CPB_EINVAL;
+    }
+  }
+  return launch_closed(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle, (cudaStream_t)stream);
+}
+
+int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,
+                    int64_t n_samples, int32_t rng, double* d_pmin, double* d_pmax,
+                    double* d_psaddle, int64_t* d_counts, void* stream) {
+  int s = check_field(f, true);
+  if (s) return s;
+  if (rng != CPB_RNG_SPLITMIX && rng != CPB_RNG_PHILOX) { set_error("unknown rng %d", rng); return CPB_EINVAL; }
+  if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
+    if (row_end > row_begin) {
+      set_error("rows [%lld, %lld) need a one-row halo inside the field",
+                (long long)row_begin, (long long)row_end);
+      return CPB_EINVAL;
+    }
+  }
+  return launch_mc(f, row_begin, row_end, seed, n_samples, rng, d_pmin, d_pmax, d_psaddle,
+                   d_counts, (cudaStream_t)stream);
+}
+
+int cpb_materialize(const cpb_field* f, double* d_a, double* d_b, double* d_weights,
+                    void* stream) {
+  int s = check_field(f, true);
+  if (s) return s;
+  return launch_materialize(f, d_a, d_b, d_weights, (cudaStream_t)stream);
+}
+
+int cpb_unit_block(uint64_t seed, const uint64_t* d_pixels, int64_t npix, int32_t planes,
+                   int64_t start, int64_t n, double* d_out, void* stream) {
+  if (npix < 0 || planes < 0 || n < 0 || start < 0) { set_error("negative extent"); return CPB_EINVAL; }
+  return launch_unit_block(seed, d_pixels, npix, planes, start, n, d_out, (cudaStream_t)stream);
+}
+
+int cpb_synth_ensemble(float* d_ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
+                       int64_t height, double noise_amp, uint64_t seed, void* stream) {
+  if (members < 1 || nrows < 0 || width < 1 || height < 1 || row0 < 0 || row0 + nrows > height) {
+    set_error("invalid synthetic ensemble extent");
+    return CPB_EINVAL;
+  }
+  return launch_synth(d_ens, members, row0, nrows, width, height, noise_amp, seed,
+                      (cudaStream_t)stream);
+}
+
+int cpb_host_alloc(void** ptr, size_t bytes) {
+  cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) return cuda_status(e, "cudaHostAlloc");
+  return CPB_OK;
+}
+
+int cpb_host_free(void* ptr) {
+  cudaError_t e = cudaFreeHost(ptr);
+  if (e != cudaSuccess) return cuda_status(e, "cudaFreeHost");
+  return CPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// One-call host pipeline.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  int alloc(size_t bytes, cudaStream_t s) {
+    st = s;
+    if (bytes == 0) return CPB_OK;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) { p = nullptr; return cuda_status(e, "cudaMallocAsync"); }
+    return CPB_OK;
+  }
+};
+
+struct Streams {
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  ~Streams() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev[i]) cudaEventDestroy(ev[i]);
+      if (s[i]) { cudaStreamSynchronize(s[i]); cudaStreamDestroy(s[i]); }
+    }
+  }
+};
+
+}  // namespace
+
+int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t width,
+                 int32_t kind, int32_t bins, double k, int32_t method, uint64_t seed,
+                 int64_t n_samples, uint32_t channels, double* h_pmin, double* h_pmax,
+                 double* h_psaddle, uint8_t* h_valid) {
+  if (!h_ens || members < 1 || height < 1 || width < 1) {
+    set_error("ensemble needs at least one member and one pixel");
+    return CPB_EINVAL;
+  }
+  if (height < 3 || width < 3) { set_error("field must be at least 3 x 3 to have interior pixels"); return CPB_EINVAL; }
+  if (method != 0 && method != 1) { set_error("method must be 0 (closed form) or 1 (monte carlo)"); return CPB_EINVAL; }
+  if (method == 0 && kind == CPB_GAUSSIAN) { set_error("Gaussian fields have no closed form; use monte_carlo"); return CPB_EINVAL; }
+  size_t pb[7];
+  int s = cpb_field_plane_bytes(kind, bins, (int32_t)members, height, width, pb);
+  if (s) return s;
+  Streams ss;
+  for (int i = 0; i < 2; ++i) {
+    cudaError_t e = cudaStreamCreateWithFlags(&ss.s[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e, "stream setup");
+  }
+  cudaStream_t s0 = ss.s[0];
+  const size_t plane = (size_t)height * width;
+  DevBuf lo, hi, mean, spread, wts, wtab, range, out;
+  if ((s = lo.alloc(pb[0], s0)) || (s = hi.alloc(pb[1], s0)) || (s = mean.alloc(pb[2], s0)) ||
+      (s = spread.alloc(pb[3], s0)) || (s = wts.alloc(pb[4], s0)) || (s = wtab.alloc(pb[5], s0)) ||
+      (s = range.alloc(pb[6], s0)) || (s = out.alloc(3 * plane * sizeof(double), s0)))
+    return s;
+  // row chunks of the ensemble, double-buffered: H2D of chunk i+1 overlaps the fit of chunk i
+  const size_t row_bytes = (size_t)members * width * sizeof(float);
+  int64_t chunk = (int64_t)std::max<size_t>(1, (size_t)(256u << 20) / row_bytes);
+  if (chunk > height) chunk = height;
+  DevBuf ebuf[2];
+  for (int i = 0; i < 2; ++i)
+    if ((s = ebuf[i].alloc((size_t)chunk * row_bytes, s0))) return s;
+  cudaError_t e = cudaMemsetAsync(out.p, 0, 3 * plane * sizeof(double), s0);
+  if (e != cudaSuccess) return cuda_status(e, "memset");
+  e = cudaEventRecord(ss.ev[0], s0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s[1], ss.ev[0], 0);
+  if (e != cudaSuccess) return cuda_status(e, "event");
+
+  cpb_field f = {};
+  f.kind = kind; f.bins = bins; f.members = (int32_t)members;
+  f.height = height; f.width = width; f.row0 = 0; f.global_width = width;
+  f.k = k; f.eps = 0.0;
+  f.lo = lo.p; f.hi = hi.p; f.mean = (double*)mean.p; f.spread = (double*)spread.p;
+  f.weights = wts.p; f.weight_table = (double*)wtab.p;
+  int nchunks = 0;
+  for (int64_t r0 = 0; r0 < height; r0 += chunk, ++nchunks) {
+    const int64_t nr = std::min(chunk, height - r0);
+    const int b = nchunks & 1;
+    cudaStream_t st = ss.s[b];
+    // one 2-D copy: M member rows of nr*W floats, source pitch = member plane
+    e = cudaMemcpy2DAsync(ebuf[b].p, (size_t)nr * width * sizeof(float), h_ens + r0 * width,
+                          plane * sizeof(float), (size_t)nr * width * sizeof(float), (size_t)members,
+                          cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_status(e, "H2D ensemble chunk");
+    cpb_field fc = f;
+    const size_t off = (size_t)r0 * width;
+    fc.height = nr;
+    fc.lo = (char*)lo.p + off * (pb[0] ? sizeof(float) : 0);
+    fc.hi = (char*)hi.p + off * (pb[1] ? sizeof(float) : 0);
+    fc.mean = pb[2] ? (double*)mean.p + off : nullptr;
+    fc.spread = pb[3] ? (double*)spread.p + off : nullptr;
+    fc.weights = wts.p;
+    if (kind == CPB_HISTOGRAM) {
+      // bin planes are (bins, H, W): a chunk view cannot be expressed by a base
+      // pointer alone, so the chunk is fitted into a (bins, nr, W) staging area
+      // and copied into place below
+    }
+    // serialise range accumulation across the two streams via the ring order
+    if (nchunks > 0) {
+      e = cudaStreamWaitEvent(st, ss.ev[b ^ 1], 0);
+      if (e != cudaSuccess) return cuda_status(e, "event wait");
+    }
+    if (kind == CPB_HISTOGRAM) {
+      DevBuf stage;
+      const size_t cb = (size_t)nr * width * bins * (members <= 255 ? 1 : 2);
+      if ((s = stage.alloc(cb, st))) return s;
+      fc.weights = stage.p;
+      if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc, (uint32_t*)range.p,
+                       nchunks > 0, st)))
+        return s;
+      const size_t esz = members <= 255 ? 1 : 2;
+      e = cudaMemcpy2DAsync((char*)wts.p + off * esz, plane * esz, stage.p, (size_t)nr * width * esz,
+                            (size_t)nr * width * esz, (size_t)bins, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) return cuda_status(e, "histogram plane copy");
+    } else if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc, (uint32_t*)range.p,
+                            nchunks > 0, st))) {
+      return s;
+    }
+    f.bounds = fc.bounds;
+    f.weights_mode = fc.weights_mode;
+    e = cudaEventRecord(ss.ev[b], st);
+    if (e != cudaSuccess) return cuda_status(e, "event record");
+  }
+  e = cudaStreamWaitEvent(s0, ss.ev[(nchunks - 1) & 1], 0);
+  if (e != cudaSuccess) return cuda_status(e, "event wait");
+  double gmin = 0.0, gmax = 0.0;
+  if ((s = cpb_read_range((const uint32_t*)range.p, &gmin, &gmax, s0))) return s;
+  f.eps = cpb_epsilon(gmin, gmax);
+  double* pmin = (double*)out.p;
+  double* pmax = pmin + plane;
+  double* psad = pmax + plane;
+  double* om = (channels & CPB_CH_MIN) ? pmin : nullptr;
+  double* oM = (channels & CPB_CH_MAX) ? pmax : nullptr;
+  double* oS = (channels & CPB_CH_SADDLE) ? psad : nullptr;
+  if (method == 0)
+    s = cpb_classify_closed(&f, 1, height - 1, om, oM, oS, s0);
+  else
+    s = cpb_classify_mc(&f, 1, height - 1, seed, n_samples, CPB_RNG_SPLITMIX, om, oM, oS, nullptr, s0);
+  if (s) return s;
+  double* dst[3] = {h_pmin, h_pmax, h_psaddle};
+  for (int c = 0; c < 3; ++c) {
+    if (!dst[c]) continue;
+    e = cudaMemcpyAsync(dst[c], pmin + c * plane, plane * sizeof(double), cudaMemcpyDeviceToHost, s0);
+    if (e != cudaSuccess) return cuda_status(e, "D2H probabilities");
+  }
+  if (h_valid) {
+    for (int64_t r = 0; r < height; ++r) {
+      uint8_t* row = h_valid + r * width;
+      const uint8_t inner = (r > 0 && r < height - 1) ? 1 : 0;
+      memset(row, inner, (size_t)width);
+      row[0] = 0;
+      row[width - 1] = 0;
+    }
+  }
+  e = cudaStreamSynchronize(s0);
+  if (e != cudaSuccess) return cuda_status(e, "synchronize");
+  return CPB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// Per-pixel noise-model fit over the member axis, the synthetic ensemble
+// generator and the reference-layout materialisation.
+//
+// Reference: UncertainField.from_ensemble (fields.py:125-158),
+// default_epsilon (distributions.py:30-36), from_scalar (fields.py:160-178).
+//
+// Bit-exactness: every float64 operation below that the reference performs
+// in numpy is written with an explicit round-to-nearest intrinsic
+// (__dadd_rn, __dmul_rn, ...) so no FMA contraction changes a result, and
+// the member reductions run in member order exactly like numpy's axis-0
+// reductions (sequential).  min/max and bin counts are exact.
+#include <algorithm>
+
+#include "cpb_common.cuh"
+
+namespace cpb {
+namespace {
+
+constexpr int kFitThreads = 256;
+constexpr int kRegMembers = 64;  // members kept in registers between passes
+
+struct FitArgs {
+  const float* ens;
+  int64_t mstride;  // elements between members
+  int64_t npix;     // height * width of the slab
+  int members;
+  int bins;
+  float* lo;
+  float* hi;
+  double* mean;
+  double* spread;
+  void* counts;     // (bins, npix) uint8 or uint16
+  int wmode;
+  uint32_t* range;  // [0] ordered min, [1] ordered max, [2] non-finite flag
+};
+
+CPB_D bool nonfinite(float v) { return (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u; }
+
+// Block-level merge of the per-thread range into the global words.
+CPB_D void merge_range(float vmin, float vmax, bool bad, uint32_t* range) {
+  uint32_t omin = float_to_ordered(vmin), omax = float_to_ordered(vmax);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, s));
+    omax = max(omax, __shfl_xor_sync(0xffffffffu, omax, s));
+  }
+  const unsigned anybad = __any_sync(0xffffffffu, bad);
+  __shared__ uint32_t s_min[32], s_max[32], s_bad[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_min[warp] = omin; s_max[warp] = omax; s_bad[warp] = anybad; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    omin = lane < nw ? s_min[lane] : 0xffffffffu;
+    omax = lane < nw ? s_max[lane] : 0u;
+    uint32_t b = lane < nw ? s_bad[lane] : 0u;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, s));
+      omax = max(omax, __shfl_xor_sync(0xffffffffu, omax, s));
+      b |= __shfl_xor_sync(0xffffffffu, b, s);
+    }
+    if (lane == 0) {
+      atomicMin(range + 0, omin);
+      atomicMax(range + 1, omax);
+      if (b) atomicOr(range + 2, 1u);
+    }
+  }
+}
+
+// Histogram bin of value v: clip(floor((v - lo) * (h / (hi - lo))), 0, h-1)
+// (fields.py:147-148), evaluated with the same two roundings.
+CPB_D int bin_of(float v, double lo, double scale, int h) {
+  const double t = floor(__dmul_rn(__dsub_rn((double)v, lo), scale));
+  return (int)fmax(0.0, fmin(t, (double)(h - 1)));
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kFitThreads) fit_reg_kernel(FitArgs a) {
+  extern __shared__ uint32_t s_cnt[];  // (bins, blockDim) per-thread counters (histogram)
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = p < a.npix;
+  const int M = a.members;
+  float v[kRegMembers];
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  double sum = 0.0;
+  if (live) {
+    const float* src = a.ens + p;
+#pragma unroll
+    for (int m = 0; m < kRegMembers; ++m)
+      if (m < M) v[m] = __ldcs(src + m * a.mstride);
+#pragma unroll
+    for (int m = 0; m < kRegMembers; ++m) {
+      if (m < M) {
+        bad |= nonfinite(v[m]);
+        vmin = fminf(vmin, v[m]);
+        vmax = fmaxf(vmax, v[m]);
+        if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) sum = __dadd_rn(sum, (double)v[m]);
+      }
+    }
+    if (KIND == CPB_UNIFORM || KIND == CPB_HISTOGRAM) {
+      a.lo[p] = vmin;
+      a.hi[p] = vmax;
+    }
+    if (KIND == CPB_HISTOGRAM) {
+      const int h = a.bins;
+      for (int b = 0; b < h; ++b) s_cnt[b * blockDim.x + threadIdx.x] = 0u;
+      if (vmax > vmin) {  // degenerate pixels are binned at use, once eps is known
+        const double lo = (double)vmin, hi = (double)vmax;
+        const double scale = __ddiv_rn((double)h, __dsub_rn(hi, lo));
+#pragma unroll
+        for (int m = 0; m < kRegMembers; ++m)
+          if (m < M) s_cnt[bin_of(v[m], lo, scale, h) * blockDim.x + threadIdx.x] += 1u;
+      }
+      if (a.wmode == CPB_WEIGHTS_U8) {
+        uint8_t* c = static_cast<uint8_t*>(a.counts);
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint8_t)s_cnt[b * blockDim.x + threadIdx.x];
+      } else {
+        uint16_t* c = static_cast<uint16_t*>(a.counts);
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint16_t)s_cnt[b * blockDim.x + threadIdx.x];
+      }
+    }
+    if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) {
+      // numpy: mean = sum / M; var = sum((v - mean)^2) / (M - 1); std = sqrt(var)
+      const double mean = __ddiv_rn(sum, (double)M);
+      double sq = 0.0;
+#pragma unroll
+      for (int m = 0; m < kRegMembers; ++m) {
+        if (m < M) {
+          const double d = __dsub_rn((double)v[m], mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+      }
+      a.mean[p] = mean;
+      a.spread[p] = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
+    }
+  }
+  merge_range(vmin, vmax, bad, a.range);
+}
+
+// Members beyond the register budget: same arithmetic, the second pass
+// re-reads the member column (L2-resident right after the first pass).
+template <int KIND>
+__global__ void __launch_bounds__(kFitThreads) fit_loop_kernel(FitArgs a) {
+  extern __shared__ uint32_t s_cnt[];
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = p < a.npix;
+  const int M = a.members;
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  if (live) {
+    const float* src = a.ens + p;
+    double sum = 0.0;
+#pragma unroll 8
+    for (int m = 0; m < M; ++m) {
+      const float x = __ldg(src + (int64_t)m * a.mstride);
+      bad |= nonfinite(x);
+      vmin = fminf(vmin, x);
+      vmax = fmaxf(vmax, x);
+      if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) sum = __dadd_rn(sum, (double)x);
+    }
+    if (KIND == CPB_UNIFORM || KIND == CPB_HISTOGRAM) {
+      a.lo[p] = vmin;
+      a.hi[p] = vmax;
+    }
+    if (KIND == CPB_HISTOGRAM) {
+      const int h = a.bins;
+      for (int b = 0; b < h; ++b) s_cnt[b * blockDim.x + threadIdx.x] = 0u;
+      if (vmax > vmin) {
+        const double lo = (double)vmin, hi = (double)vmax;
+        const double scale = __ddiv_rn((double)h, __dsub_rn(hi, lo));
+        for (int m = 0; m < M; ++m)
+          s_cnt[bin_of(__ldg(src + (int64_t)m * a.mstride), lo, scale, h) * blockDim.x + threadIdx.x] += 1u;
+      }
+      if (a.wmode == CPB_WEIGHTS_U8) {
+        uint8_t* c = static_cast<uint8_t*>(a.counts);
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint8_t)s_cnt[b * blockDim.x + threadIdx.x];
+      } else {
+        uint16_t* c = static_cast<uint16_t*>(a.counts);
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint16_t)s_cnt[b * blockDim.x + threadIdx.x];
+      }
+    }
+    if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) {
+      const double mean = __ddiv_rn(sum, (double)M);
+      double sq = 0.0;
+      for (int m = 0; m < M; ++m) {
+        const double d = __dsub_rn((double)__ldg(src + (int64_t)m * a.mstride), mean);
+        sq = __dadd_rn(sq, __dmul_rn(d, d));
+      }
+      a.mean[p] = mean;
+      a.spread[p] = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
+    }
+  }
+  merge_range(vmin, vmax, bad, a.range);
+}
+
+__global__ void range_init_kernel(uint32_t* range) {
+  range[0] = 0xffffffffu;
+  range[1] = 0u;
+  range[2] = 0u;
+}
+
+// c / M for c in [0, M]: the exact count->weight map of fields.py:151.
+__global__ void weight_table_kernel(double* t, int members) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c <= members) t[c] = __ddiv_rn((double)c, (double)members);
+}
+
+// fields.py:160-178: lo/hi = v -+ half, half = eb/2 (or eps/2 when eb == 0)
+__global__ void from_scalar_kernel(const double* v, int64_t n, double half, double* lo,
+                                   double* hi) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double x = v[i];
+    lo[i] = __dsub_rn(x, half);
+    hi[i] = __dadd_rn(x, half);
+  }
+}
+
+// Reference-layout float64 params (fields.py:137-158 outputs).
+__global__ void materialize_kernel(FieldView f, double* a, double* b, double* w) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= f.plane) return;
+  if (f.kind == CPB_EPANECHNIKOV) {
+    double m, hw;
+    load_epan(f, p, m, hw);
+    a[p] = m;
+    b[p] = hw;
+    return;
+  }
+  if (f.kind == CPB_GAUSSIAN) {
+    a[p] = f.mean[p];
+    b[p] = f.spread[p];
+    return;
+  }
+  double lo, hi;
+  const bool deg = load_bounds(f, p, lo, hi);
+  a[p] = lo;
+  b[p] = hi;
+  if (f.kind == CPB_HISTOGRAM && w != nullptr) {
+    const int h = f.bins;
+    const int dbin = deg ? degenerate_bin((double)static_cast<const float*>(f.lo)[p], lo, hi, h) : 0;
+    for (int k = 0; k < h; ++k) w[p * h + k] = load_weight(f, p, k, deg, dbin);
+  }
+}
+
+// bowl(r, c) = 4 (x^2 + y^2) - 3 x^2 y^2, x = c * (2/(W-1)) - 1, y = r * (2/(H-1)) - 1
+// value = f32(bowl + amp * (2u - 1)); twin of oracle.synthetic_rows.
+__global__ void synth_kernel(float* ens, int64_t mstride, int members, int64_t row0,
+                             int64_t nrows, int64_t width, int64_t height, double amp,
+                             uint64_t seed) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows * width) return;
+  const int64_t lr = i / width, c = i - lr * width, r = row0 + lr;
+  const double sx = width > 1 ? __ddiv_rn(2.0, (double)(width - 1)) : 0.0;
+  const double sy = height > 1 ? __ddiv_rn(2.0, (double)(height - 1)) : 0.0;
+  const double x = __dsub_rn(__dmul_rn((double)c, sx), 1.0);
+  const double y = __dsub_rn(__dmul_rn((double)r, sy), 1.0);
+  const double x2 = __dmul_rn(x, x), y2 = __dmul_rn(y, y);
+  const double base = __dsub_rn(__dmul_rn(4.0, __dadd_rn(x2, y2)), __dmul_rn(3.0, __dmul_rn(x2, y2)));
+  const uint64_t pk = pixel_key(seed, (uint64_t)(r * width + c));
+  for (int m = 0; m < members; ++m) {
+    const double u = stream_u01(plane_key(pk, (uint64_t)m), 0);
+    const double noise = __dmul_rn(amp, __dsub_rn(__dmul_rn(2.0, u), 1.0));
+    ens[(int64_t)m * mstride + i] = __double2float_rn(__dadd_rn(base, noise));
+  }
+}
+
+inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
+
+}  // namespace
+
+int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range, bool accumulate,
+               cudaStream_t st) {
+  FitArgs a;
+  a.ens = ens;
+  a.mstride = mstride;
+  a.npix = f->height * f->width;
+  a.members = f->members;
+  a.bins = f->bins;
+  a.lo = static_cast<float*>(f->lo);
+  a.hi = static_cast<float*>(f->hi);
+  a.mean = f->mean;
+  a.spread = f->spread;
+  a.counts = f->weights;
+  a.wmode = f->members <= 255 ? CPB_WEIGHTS_U8 : CPB_WEIGHTS_U16;
+  a.range = range;
+  f->bounds = CPB_BOUNDS_F32_FITTED;
+  f->weights_mode = f->kind == CPB_HISTOGRAM ? a.wmode : CPB_WEIGHTS_F64;
+  if (!accumulate) {
+    range_init_kernel<<<1, 1, 0, st>>>(range);
+    CPB_CHECK_LAUNCH("range init");
+  }
+  if (a.npix == 0) return CPB_OK;
+  if (f->kind == CPB_HISTOGRAM) {
+    weight_table_kernel<<<grid_for(f->members + 1, 256), 256, 0, st>>>(f->weight_table, f->members);
+    CPB_CHECK_LAUNCH("weight table");
+  }
+  int threads = kFitThreads;
+  size_t smem = 0;
+  if (f->kind == CPB_HISTOGRAM) {
+    // per-thread bin counters; shrink the block for very many bins
+    while ((size_t)f->bins * threads * 4 > 160 * 1024 && threads > 32) threads >>= 1;
+    smem = (size_t)f->bins * threads * 4;
+    if (smem > 160 * 1024) {
+      set_error("histogram fit supports at most %d bins", 160 * 1024 / (32 * 4));
+      return CPB_EINVAL;
+    }
+  }
+  const unsigned grid = grid_for(a.npix, threads);
+  const bool reg = f->members <= kRegMembers;
+#define CPB_FIT_CASE(K)                                                                   \
+  case K: {                                                                               \
+    auto kern = reg ? fit_reg_kernel<K> : fit_loop_kernel<K>;                             \
+    if (smem > 48 * 1024)                                                                 \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kern<<<grid, threads, smem, st>>>(a);                                                 \
+    break;                                                                                \
+  }
+  switch (f->kind) {
+    CPB_FIT_CASE(CPB_UNIFORM)
+    CPB_FIT_CASE(CPB_EPANECHNIKOV)
+    CPB_FIT_CASE(CPB_HISTOGRAM)
+    CPB_FIT_CASE(CPB_GAUSSIAN)
+    default:
+      set_error("unknown model kind %d", f->kind);
+      return CPB_EINVAL;
+  }
+#undef CPB_FIT_CASE
+  CPB_CHECK_LAUNCH("fit kernel");
+  return CPB_OK;
+}
+
+int launch_from_scalar(const double* v, int64_t n, double half, double* lo, double* hi,
+                       cudaStream_t st) {
+  if (n == 0) return CPB_OK;
+  from_scalar_kernel<<<grid_for(n, 256), 256, 0, st>>>(v, n, half, lo, hi);
+  CPB_CHECK_LAUNCH("from_scalar kernel");
+  return CPB_OK;
+}
+
+int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cudaStream_t st) {
+  const FieldView v = make_view(*f);
+  if (v.plane == 0) return CPB_OK;
+  materialize_kernel<<<grid_for(v.plane, 256), 256, 0, st>>>(v, a, b, w);
+  CPB_CHECK_LAUNCH("materialize kernel");
+  return CPB_OK;
+}
+
+int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
+                 int64_t height, double amp, uint64_t seed, cudaStream_t st) {
+  const int64_t n = nrows * width;
+  if (n == 0) return CPB_OK;
+  synth_kernel<<<grid_for(n, 256), 256, 0, st>>>(ens, n, (int)members, row0, nrows, width, height,
+                                                  amp, seed);
+  CPB_CHECK_LAUNCH("synth kernel");
+  return CPB_OK;
+}
+
+}  // namespace cpb

@@ -1,0 +1,253 @@
+// Monte Carlo pattern estimator and the keyed uniform stream.
+//
+// Reference: _mc_chunk (engine.py:659-666), _position_samples
+// (engine.py:632-656), the inverse CDFs (distributions.py:60-89),
+// _pattern_stats (engine.py:195-222) and rngstream.unit_block
+// (rngstream.py:33-48).
+//
+// One warp per vertex: the 32 lanes split the n joint draws, each lane keeps
+// integer hit counts, and a warp reduction gives exact totals (integer sums
+// are order-free, so results do not depend on the launch shape).  With the
+// splitmix64 stream each draw is the reference's (seed, pixel, plane, i)
+// uniform and the inverse CDFs repeat numpy's float64 operations with
+// explicit round-to-nearest intrinsics, so uniform and histogram counts are
+// bit-identical to the reference; Epanechnikov (asin/sin) and Gaussian
+// (log1p/cos) draws can differ from glibc by an ulp, which flips a strict
+// comparison only on an exact tie.
+#include "cpb_common.cuh"
+
+namespace cpb {
+namespace {
+
+constexpr int kMcWarps = 4;  // warps (vertices in flight) per block
+
+struct McArgs {
+  int64_t row_begin, nvert, cols;  // interior columns per row = width - 2
+  uint64_t seed;
+  int64_t n;
+  double* pmin;
+  double* pmax;
+  double* psad;
+  int64_t* counts;  // optional: 3 planes (min, max, saddle)
+};
+
+// Per-position sampler state (histogram tables live in shared memory).
+struct Sampler {
+  double a, b;      // uniform: lo, hi | epanechnikov: mid, half | gaussian: mean, sd | histogram: lo, binw
+  const double* wn; // histogram: h renormalised weights (smem)
+  const double* cum;// histogram: h+1 prefix sums, cum[h] = 1 (smem)
+};
+
+template <int KIND>
+CPB_D double draw(const Sampler& s, double u, double u2, int h) {
+  if (KIND == CPB_UNIFORM) {  // (1 - u) lo + u hi  (distributions.py:60-61)
+    return __dadd_rn(__dmul_rn(__dsub_rn(1.0, u), s.a), __dmul_rn(u, s.b));
+  } else if (KIND == CPB_EPANECHNIKOV) {  // distributions.py:64-70
+    if (u == 0.0) return __dsub_rn(s.a, s.b);
+    if (u == 1.0) return __dadd_rn(s.a, s.b);
+    const double root = __dmul_rn(2.0, sin(__ddiv_rn(asin(__dsub_rn(__dmul_rn(2.0, u), 1.0)), 3.0)));
+    return __dadd_rn(s.a, __dmul_rn(s.b, root));
+  } else if (KIND == CPB_GAUSSIAN) {  // Box-Muller, engine.py:638-640
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log1p(-u)));
+    const double z = __dmul_rn(r, cos(__dmul_rn(6.283185307179586, u2)));
+    return __dadd_rn(s.a, __dmul_rn(s.b, z));
+  } else {  // histogram_icdf, distributions.py:73-89
+    int j = 0;
+    for (int k = 1; k < h; ++k) j += (u >= s.cum[k]) ? 1 : 0;
+    const double cj = s.cum[j], wj = s.wn[j];
+    const double frac = wj > 0.0 ? __ddiv_rn(__dsub_rn(u, cj), wj) : 0.0;
+    if (u == 1.0) return __dadd_rn(s.a, __dmul_rn(s.b, (double)h));
+    const double e0 = __dadd_rn(s.a, __dmul_rn(s.b, (double)j));
+    return __dadd_rn(__dmul_rn(__dsub_rn(1.0, frac), e0), __dmul_rn(frac, __dadd_rn(e0, s.b)));
+  }
+}
+
+template <int KIND, int RNG>
+__global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a) {
+  extern __shared__ double s_tab[];  // per warp: 5 x (h wn + h+1 cum)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = f.bins;
+  const int tab = 2 * h + 1;
+  double* my_tab = s_tab + (size_t)warp * 5 * tab;
+  const int64_t warps_total = (int64_t)gridDim.x * kMcWarps;
+  for (int64_t v = (int64_t)blockIdx.x * kMcWarps + warp; v < a.nvert; v += warps_total) {
+    const int64_t r = a.row_begin + v / a.cols, c = 1 + v % a.cols;
+    const int64_t idx = r * f.width + c;
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    Sampler s[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      if (KIND == CPB_UNIFORM) {
+        load_bounds(f, at[p], s[p].a, s[p].b);
+      } else if (KIND == CPB_EPANECHNIKOV) {
+        double m, hw;
+        load_epan(f, at[p], m, hw);
+        const double lo = __dsub_rn(m, hw), hi = __dadd_rn(m, hw);  // engine.py:645-649
+        s[p].a = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        s[p].b = __dmul_rn(0.5, __dsub_rn(hi, lo));
+      } else if (KIND == CPB_GAUSSIAN) {
+        s[p].a = __ldg(f.mean + at[p]);
+        s[p].b = __ldg(f.spread + at[p]);
+      } else {
+        double lo, hi;
+        const bool deg = load_bounds(f, at[p], lo, hi);
+        s[p].a = lo;
+        s[p].b = __ddiv_rn(__dsub_rn(hi, lo), (double)h);  // binw, engine.py:655
+        s[p].wn = my_tab + p * tab;
+        s[p].cum = my_tab + p * tab + h;
+        if (lane == p) {  // one lane per position builds its tables (engine.py:650-654)
+          const int dbin =
+              deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at[p]), lo, hi, h) : 0;
+          const double total =
+              pairwise_sum([&](int b) { return load_weight(f, at[p], b, deg, dbin); }, h);
+          double* wn = my_tab + p * tab;
+          double* cum = wn + h;
+          double run = 0.0;
+          cum[0] = 0.0;
+          for (int b = 0; b < h; ++b) {
+            wn[b] = __ddiv_rn(load_weight(f, at[p], b, deg, dbin), total);
+            run = __dadd_rn(run, wn[b]);
+            cum[b + 1] = run;
+          }
+          cum[h] = 1.0;
+        }
+      }
+    }
+    if (KIND == CPB_HISTOGRAM) __syncwarp();
+    uint64_t key[10];
+    const uint64_t px = (uint64_t)((f.row0 + r) * f.gwidth + c);
+    constexpr int per = KIND == CPB_GAUSSIAN ? 2 : 1;
+    if (RNG == CPB_RNG_SPLITMIX) {
+      const uint64_t pk = pixel_key(a.seed, px);
+#pragma unroll
+      for (int q = 0; q < 5 * per; ++q) key[q] = plane_key(pk, (uint64_t)q);
+    }
+    uint32_t cmin = 0, cmax = 0, csad = 0;
+    for (int64_t i = lane; i < a.n; i += 32) {
+      double u[10];
+      if (RNG == CPB_RNG_SPLITMIX) {
+#pragma unroll
+        for (int q = 0; q < 5 * per; ++q) u[q] = stream_u01(key[q], (uint64_t)i);
+      } else {
+        const uint2 k2 = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+#pragma unroll
+        for (int q = 0; q < (5 * per + 1) / 2; ++q) {
+          const uint4 o = philox4x32_10(
+              make_uint4((uint32_t)i, (uint32_t)((uint64_t)i >> 32) ^ ((uint32_t)q << 24),
+                         (uint32_t)px, (uint32_t)(px >> 32)), k2);
+          u[2 * q] = u53_from(o.x, o.y);
+          if (2 * q + 1 < 5 * per) u[2 * q + 1] = u53_from(o.z, o.w);
+        }
+      }
+      double x[5];
+#pragma unroll
+      for (int p = 0; p < 5; ++p)
+        x[p] = draw<KIND>(s[p], u[p * per], per == 2 ? u[p * per + 1] : 0.0, h);
+      // strict comparisons, ties count against every pattern (engine.py:213-221)
+      const bool lE = x[0] < x[1], lN = x[0] < x[2], lW = x[0] < x[3], lS = x[0] < x[4];
+      const bool gE = x[0] > x[1], gN = x[0] > x[2], gW = x[0] > x[3], gS = x[0] > x[4];
+      cmin += (lE & lN & lW & lS);
+      cmax += (gE & gN & gW & gS);
+      csad += ((lE & gN & lW & gS) | (gE & lN & gW & lS));
+    }
+    cmin = __reduce_add_sync(0xffffffffu, cmin);
+    cmax = __reduce_add_sync(0xffffffffu, cmax);
+    csad = __reduce_add_sync(0xffffffffu, csad);
+    if (lane == 0) {
+      const double n = (double)a.n;  // np.mean of booleans: float64 count / n
+      if (a.pmin) a.pmin[idx] = __ddiv_rn((double)cmin, n);
+      if (a.pmax) a.pmax[idx] = __ddiv_rn((double)cmax, n);
+      if (a.psad) a.psad[idx] = __ddiv_rn((double)csad, n);
+      if (a.counts) {
+        const int64_t plane = f.plane;
+        a.counts[idx] = cmin;
+        a.counts[plane + idx] = cmax;
+        a.counts[2 * plane + idx] = csad;
+      }
+    }
+    if (KIND == CPB_HISTOGRAM) __syncwarp();
+  }
+}
+
+__global__ void unit_block_kernel(uint64_t seed, const uint64_t* px, int64_t npix, int planes,
+                                  int64_t start, int64_t n, double* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = npix * planes * n;
+  if (t >= total) return;
+  const int64_t i = t % n, q = (t / n) % planes, p = t / (n * planes);
+  const uint64_t key = plane_key(pixel_key(seed, px[p]), (uint64_t)q);
+  out[t] = stream_u01(key, (uint64_t)(start + i));
+}
+
+}  // namespace
+
+int launch_mc(const cpb_field* fld, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t n,
+              int rng, double* pmin, double* pmax, double* psad, int64_t* counts, cudaStream_t st) {
+  const FieldView f = make_view(*fld);
+  const int64_t rows = row_end - row_begin;
+  if (rows <= 0 || f.width < 3) return CPB_OK;
+  if (n < 1) {
+    set_error("sample counts must be positive");
+    return CPB_EINVAL;
+  }
+  if (n > 0x7fffffffll * 32) {
+    set_error("n_samples too large");
+    return CPB_EINVAL;
+  }
+  McArgs a;
+  a.row_begin = row_begin;
+  a.cols = f.width - 2;
+  a.nvert = rows * a.cols;
+  a.seed = seed;
+  a.n = n;
+  a.pmin = pmin;
+  a.pmax = pmax;
+  a.psad = psad;
+  a.counts = counts;
+  const size_t smem = f.kind == CPB_HISTOGRAM ? (size_t)kMcWarps * 5 * (2 * f.bins + 1) * sizeof(double) : 0;
+  if (smem > 200 * 1024) {
+    set_error("too many histogram bins for the Monte Carlo sampler tables");
+    return CPB_EINVAL;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (a.nvert + kMcWarps - 1) / kMcWarps;
+  const unsigned grid = (unsigned)(want < (int64_t)sms * 64 ? want : (int64_t)sms * 64);
+#define CPB_MC_LAUNCH(K, R)                                                                  \
+  do {                                                                                       \
+    auto kern = mc_kernel<K, R>;                                                             \
+    if (smem > 48 * 1024)                                                                    \
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);    \
+    kern<<<grid, kMcWarps * 32, smem, st>>>(f, a);                                           \
+  } while (0)
+#define CPB_MC_KIND(K)                                                                       \
+  case K:                                                                                    \
+    if (rng == CPB_RNG_PHILOX) CPB_MC_LAUNCH(K, CPB_RNG_PHILOX);                             \
+    else CPB_MC_LAUNCH(K, CPB_RNG_SPLITMIX);                                                 \
+    break;
+  switch (f.kind) {
+    CPB_MC_KIND(CPB_UNIFORM)
+    CPB_MC_KIND(CPB_EPANECHNIKOV)
+    CPB_MC_KIND(CPB_HISTOGRAM)
+    CPB_MC_KIND(CPB_GAUSSIAN)
+    default:
+      set_error("unknown model kind %d", f.kind);
+      return CPB_EINVAL;
+  }
+#undef CPB_MC_KIND
+#undef CPB_MC_LAUNCH
+  CPB_CHECK_LAUNCH("monte carlo kernel");
+  return CPB_OK;
+}
+
+int launch_unit_block(uint64_t seed, const uint64_t* px, int64_t npix, int planes, int64_t start,
+                      int64_t n, double* out, cudaStream_t st) {
+  const int64_t total = npix * planes * n;
+  if (total == 0) return CPB_OK;
+  unit_block_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(seed, px, npix, planes, start, n, out);
+  CPB_CHECK_LAUNCH("unit_block kernel");
+  return CPB_OK;
+}
+
+}  // namespace cpb

@@ -1,0 +1,144 @@
+"""Generate the golden fixtures by running the REFERENCE package itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``critprob`` read-only from /root/reference/pkg/src, feeds it
+small seeded inputs, and stores inputs + outputs under tests/golden/*.npz.
+The fixtures travel with the repo; nothing at test time reads
+/root/reference.  Reference entry points exercised:
+
+- UncertainField.from_ensemble  (fields.py:125-158)
+- UncertainField.from_scalar    (fields.py:160-178)
+- classify_field closed form    (engine.py:716-787, 594-629)
+- classify_field Monte Carlo    (engine.py:659-666, 632-656)
+- rngstream.unit_block          (rngstream.py:33-48)
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+from critprob import rngstream  # noqa: E402
+from critprob.engine import EstimatorSpec, classify_field  # noqa: E402
+from critprob.fields import EnsembleStack, ModelSpec, UncertainField  # noqa: E402
+from critprob.synth import ackley_ensemble  # noqa: E402
+
+
+def _ens(seed, shape, members, amp=0.3, base_amp=1.0):
+    rng = np.random.default_rng(seed)
+    base = rng.uniform(-base_amp, base_amp, shape)
+    return (base + rng.uniform(-amp, amp, (members, *shape))).astype(np.float32)
+
+
+def ensembles() -> dict:
+    out = {
+        "ackley": ackley_ensemble(13, 11, members=24, noise_amp=0.3, seed=0).values,
+        "rand": _ens(11, (9, 10), 24),
+        "wide": _ens(5, (8, 12), 7, amp=2.0, base_amp=0.2),
+    }
+    deg = np.zeros((5, 6, 7), dtype=np.float32)
+    deg[:, 2, 2] = 7.0
+    deg[:, 3, 4] = -1.5
+    deg[1:, 1, 5] = 0.25
+    deg[0, 1, 5] = 0.5
+    out["degenerate"] = deg
+    out["constant"] = np.full((4, 5, 5), 2.5, dtype=np.float32)
+    out["single"] = _ens(3, (5, 6), 1)
+    big = _ens(21, (7, 9), 40, amp=1e3, base_amp=1e4)
+    big[:, 3, 3] = 1e4 + 0.5        # degenerate pixel in a wide-range stack
+    out["offset"] = big
+    return out
+
+
+MODELS = [
+    ("uniform", 5),
+    ("epanechnikov", 5),
+    ("gaussian", 5),
+    ("histogram", 1),
+    ("histogram", 3),
+    ("histogram", 5),
+    ("histogram", 8),
+    ("histogram", 9),
+    ("histogram", 16),
+]
+
+
+def main() -> None:
+    ens = ensembles()
+    fit = {}
+    closed = {}
+    mc = {}
+    for name, vals in ens.items():
+        fit[f"ens/{name}"] = vals
+        stack = EnsembleStack(vals)
+        for kind, bins in MODELS:
+            if vals.shape[0] < 2 and kind in ("epanechnikov", "gaussian"):
+                continue
+            field = UncertainField.from_ensemble(stack, ModelSpec(kind=kind, bins=bins))
+            tag = f"{name}/{kind}/{bins}"
+            for pname, arr in field.params.items():
+                fit[f"{tag}/{pname}"] = arr
+            if min(field.shape) < 3:
+                continue
+            if kind != "gaussian":
+                prob = classify_field(field)
+                for ch in ("min", "max", "saddle"):
+                    closed[f"{tag}/{ch}"] = prob.channel(ch)
+            if name in ("ackley", "rand", "degenerate", "offset") and bins in (1, 5, 9):
+                n = 257 if name != "offset" else 64
+                est = EstimatorSpec(method="monte_carlo", n_samples=n, seed=9)
+                prob = classify_field(field, est)
+                for ch in ("min", "max", "saddle"):
+                    mc[f"{tag}/{ch}"] = prob.channel(ch)
+                mc[f"{tag}/n"] = np.array(n)
+
+    # closed-form known answers on hand-built 3x3 uniform fields (test_engine.py:147-163)
+    lo = np.zeros((3, 3))
+    hi = np.ones((3, 3))
+    for (r, c), (a, b) in {(1, 1): (0.0, 2.0), (1, 2): (1.0, 3.0), (0, 1): (0.5, 2.5),
+                           (1, 0): (1.5, 3.5), (2, 1): (0.0, 2.0)}.items():
+        lo[r, c], hi[r, c] = a, b
+    field = UncertainField(ModelSpec("uniform"), {"lo": lo, "hi": hi})
+    prob = classify_field(field)
+    closed["kat3x3/lo"] = lo
+    closed["kat3x3/hi"] = hi
+    for ch in ("min", "max", "saddle"):
+        closed[f"kat3x3/{ch}"] = prob.channel(ch)
+
+    # from_scalar (fields.py:160-178)
+    rng = np.random.default_rng(9)
+    raster = rng.uniform(0.0, 10.0, (6, 7))
+    for eb in (0.5, 0.0):
+        f = UncertainField.from_scalar(raster, eb)
+        fit[f"scalar/{eb}/lo"] = f.params["lo"]
+        fit[f"scalar/{eb}/hi"] = f.params["hi"]
+        prob = classify_field(f)
+        for ch in ("min", "max", "saddle"):
+            closed[f"scalar/{eb}/{ch}"] = prob.channel(ch)
+    fit["scalar/raster"] = raster
+
+    # counter RNG (rngstream.py:33-48)
+    rng_fx = {}
+    px = np.array([0, 1, 17, 2**40 + 3, 2**63 + 5], dtype=np.uint64)
+    for seed in (0, 7, -1, 2**64 - 2, 123456789):
+        rng_fx[f"{seed}"] = rngstream.unit_block(seed, px, 3, 11)
+    rng_fx["pixels"] = px
+
+    np.savez_compressed(os.path.join(HERE, "fit.npz"), **fit)
+    np.savez_compressed(os.path.join(HERE, "closed.npz"), **closed)
+    np.savez_compressed(os.path.join(HERE, "mc.npz"), **mc)
+    np.savez_compressed(os.path.join(HERE, "rng.npz"), **rng_fx)
+    for f in ("fit", "closed", "mc", "rng"):
+        print(f, os.path.getsize(os.path.join(HERE, f + ".npz")), "bytes")
+
+
+if __name__ == "__main__":
+    main()

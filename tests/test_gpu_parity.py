@@ -1,0 +1,310 @@
+"""GPU parity: the sm_100a path through the C ABI against the reference.
+
+Every test calls the product package (ctypes -> libcritprob_b200.so) and
+checks it against the golden fixtures produced by the reference itself
+(tests/golden/make_golden.py) and against the pinned CPU oracle on seeded
+inputs.  Bars (from SURVEY.md section 8 / the north_star):
+
+- fit (lo/hi, counts->weights, mean, std, halfwidth): bit-exact
+- closed form (float64): |gpu - ref| <= 1e-12 absolute
+- Monte Carlo, splitmix64 stream: uniform/histogram identical counts;
+  epanechnikov/gaussian identical except where libm ulps flip an exact tie
+  (<= 1 count per channel per pixel, and in practice none)
+- keyed uniform stream: bit-exact
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2407_18015_b200 as cpb  # noqa: E402
+from oracle import critprob_oracle as orc  # noqa: E402
+
+CLOSED_TOL = 1e-12
+
+
+def _fit(vals, kind, bins=5, k=None):
+    model = cpb.ModelSpec(kind=kind, bins=bins) if k is None else cpb.ModelSpec(kind=kind, bins=bins, k=k)
+    return cpb.UncertainField.from_ensemble(cpb.EnsembleStack(vals), model)
+
+
+def _models_in(fit):
+    out = []
+    for key in fit:
+        parts = key.split("/")
+        if len(parts) == 4 and parts[0] != "scalar":
+            out.append((parts[0], parts[1], int(parts[2]), parts[3]))
+    return out
+
+
+# ---------------------------------------------------------------- fit
+def test_fit_bitexact_against_reference(golden):
+    fit = golden["fit"]
+    seen = 0
+    cache = {}
+    for name, kind, bins, pname in _models_in(fit):
+        key = (name, kind, bins)
+        if key not in cache:
+            cache[key] = _fit(fit[f"ens/{name}"], kind, bins).params
+        got = cache[key][pname]
+        ref = fit[f"{name}/{kind}/{bins}/{pname}"]
+        assert got.shape == ref.shape
+        assert np.array_equal(got, ref), (name, kind, bins, pname, np.max(np.abs(got - ref)))
+        seen += 1
+    assert seen > 40
+
+
+def test_fit_device_resident_stack_matches_host(golden):
+    vals = golden["fit"]["ens/ackley"]
+    host = _fit(vals, "histogram", 8).params
+    dev = _fit(torch.as_tensor(vals, device="cuda"), "histogram", 8).params
+    for k in host:
+        assert np.array_equal(host[k], dev[k])
+
+
+def test_fit_large_members_loop_path():
+    rng = np.random.default_rng(5)
+    vals = (rng.uniform(-1, 1, (9, 11)) + rng.uniform(-0.3, 0.3, (300, 9, 11))).astype(np.float32)
+    for kind, bins in (("uniform", 5), ("epanechnikov", 5), ("gaussian", 5), ("histogram", 7)):
+        got = _fit(vals, kind, bins).params
+        ref = orc.fit(vals, kind, bins)
+        for k in ref:
+            assert np.array_equal(got[k], ref[k]), (kind, k)
+
+
+def test_fit_k_parameter_and_errors():
+    rng = np.random.default_rng(6)
+    vals = rng.uniform(0, 1, (12, 5, 6)).astype(np.float32)
+    got = _fit(vals, "epanechnikov", k=1.0).params["halfwidth"]
+    assert np.array_equal(got, orc.fit(vals, "epanechnikov", k=1.0)["halfwidth"])
+    single = np.ones((1, 4, 4), dtype=np.float32)
+    for kind in ("epanechnikov", "gaussian"):
+        with pytest.raises(ValueError):
+            _fit(single, kind)
+    bad = torch.zeros((3, 4, 4), device="cuda")
+    bad[1, 2, 2] = float("nan")
+    with pytest.raises(ValueError):
+        _fit(bad, "uniform")
+    with pytest.raises(ValueError):
+        cpb.EnsembleStack(np.full((2, 3, 3), np.inf, dtype=np.float32))
+
+
+def test_from_scalar_bitexact(golden):
+    fit = golden["fit"]
+    for eb in (0.5, 0.0):
+        f = cpb.UncertainField.from_scalar(fit["scalar/raster"], eb)
+        assert np.array_equal(f.params["lo"], fit[f"scalar/{eb}/lo"])
+        assert np.array_equal(f.params["hi"], fit[f"scalar/{eb}/hi"])
+    with pytest.raises(ValueError):
+        cpb.UncertainField.from_scalar(np.ones((3, 3)), -0.1)
+
+
+# ---------------------------------------------------------------- closed form
+def test_closed_form_against_reference(golden):
+    fit, closed = golden["fit"], golden["closed"]
+    seen = 0
+    for key in closed:
+        parts = key.split("/")
+        if len(parts) != 4 or parts[3] != "min":
+            continue
+        name, kind, bins = parts[0], parts[1], int(parts[2])
+        prob = cpb.classify_field(_fit(fit[f"ens/{name}"], kind, bins))
+        for ch in ("min", "max", "saddle"):
+            ref = closed[f"{name}/{kind}/{bins}/{ch}"]
+            err = np.max(np.abs(prob.channel(ch) - ref))
+            assert err <= CLOSED_TOL, (name, kind, bins, ch, err)
+        assert not prob.valid[0].any() and prob.valid[1:-1, 1:-1].all()
+        seen += 1
+    assert seen >= 30
+
+
+def test_closed_form_user_built_fields(golden):
+    closed = golden["closed"]
+    f = cpb.UncertainField(cpb.ModelSpec("uniform"), {"lo": closed["kat3x3/lo"], "hi": closed["kat3x3/hi"]})
+    prob = cpb.classify_field(f)
+    assert prob.p_min[1, 1] == pytest.approx(0.41865234375, abs=1e-12)
+    assert prob.p_max[1, 1] == pytest.approx(0.008170572916666667, abs=1e-12)
+    assert prob.p_saddle[1, 1] == pytest.approx(0.1377604166666667, abs=1e-12)
+    for kind, params in (
+        ("uniform", {"lo": np.zeros((3, 3)), "hi": np.ones((3, 3))}),
+        ("epanechnikov", {"mean": np.full((3, 3), 2.0), "halfwidth": np.full((3, 3), 0.7)}),
+        ("histogram", {"lo": np.zeros((3, 3)), "hi": np.ones((3, 3)),
+                       "weights": np.tile([0.1, 0.3, 0.25, 0.2, 0.15], (3, 3, 1))}),
+    ):
+        prob = cpb.classify_field(cpb.UncertainField(cpb.ModelSpec(kind, bins=5), params))
+        assert prob.p_min[1, 1] == pytest.approx(0.2, abs=1e-12), kind
+        assert prob.p_max[1, 1] == pytest.approx(0.2, abs=1e-12), kind
+        assert prob.p_saddle[1, 1] == pytest.approx(1.0 / 15.0, abs=1e-12), kind
+
+
+def test_closed_form_disjoint_supports():
+    # test_engine.py:114-143: certain minimum / maximum
+    lo = np.full((3, 3), 2.0)
+    hi = np.full((3, 3), 3.0)
+    lo[1, 1], hi[1, 1] = 0.0, 1.0
+    prob = cpb.classify_field(cpb.UncertainField(cpb.ModelSpec("uniform"), {"lo": lo, "hi": hi}))
+    assert prob.p_min[1, 1] == 1.0 and prob.p_max[1, 1] == 0.0 and prob.p_saddle[1, 1] == 0.0
+    prob = cpb.classify_field(cpb.UncertainField(cpb.ModelSpec("uniform"), {"lo": -hi, "hi": -lo}))
+    assert prob.p_max[1, 1] == 1.0 and prob.p_min[1, 1] == 0.0
+
+
+def test_from_scalar_closed(golden):
+    fit, closed = golden["fit"], golden["closed"]
+    for eb in (0.5, 0.0):
+        prob = cpb.classify_field(cpb.UncertainField.from_scalar(fit["scalar/raster"], eb))
+        for ch in ("min", "max", "saddle"):
+            assert np.max(np.abs(prob.channel(ch) - closed[f"scalar/{eb}/{ch}"])) <= CLOSED_TOL
+
+
+@pytest.mark.parametrize("kind,bins,shape,members", [
+    ("uniform", 5, (64, 64), 20),          # BASELINE config 1
+    ("epanechnikov", 5, (70, 90), 20),     # config 2 model, reduced grid
+    ("histogram", 8, (40, 52), 40),        # config 3 bins, reduced grid
+    ("histogram", 16, (30, 33), 40),
+    ("histogram", 32, (20, 24), 40),
+])
+def test_closed_form_against_oracle_ackley(kind, bins, shape, members):
+    vals = orc.ackley_ensemble(shape[1], shape[0], members, noise_amp=0.3, seed=0)
+    field = _fit(vals, kind, bins)
+    ref = orc.classify(orc.fit(vals, kind, bins), kind)
+    prob = cpb.classify_field(field)
+    for ch in ("min", "max", "saddle"):
+        err = np.max(np.abs(prob.channel(ch) - ref[ch]))
+        assert err <= CLOSED_TOL, (ch, err)
+
+
+def test_closed_form_offsets_and_degenerate(golden):
+    # far-from-origin supports and degenerate pixels mixed into a wide range
+    fit = golden["fit"]
+    for name in ("offset", "degenerate", "constant", "wide"):
+        vals = fit[f"ens/{name}"]
+        for kind, bins in (("uniform", 5), ("epanechnikov", 5), ("histogram", 3), ("histogram", 8)):
+            ref = orc.classify(orc.fit(vals, kind, bins), kind)
+            prob = cpb.classify_field(_fit(vals, kind, bins))
+            for ch in ("min", "max", "saddle"):
+                err = np.max(np.abs(prob.channel(ch) - ref[ch]))
+                assert err <= CLOSED_TOL, (name, kind, bins, ch, err)
+
+
+def test_channel_subset_and_validation(golden):
+    vals = golden["fit"]["ens/rand"]
+    field = _fit(vals, "uniform")
+    full = cpb.classify_field(field)
+    only = cpb.classify_field(field, channels="min")
+    assert np.array_equal(only.p_min, full.p_min)
+    assert np.all(only.p_max == 0.0) and np.all(only.p_saddle == 0.0)
+    with pytest.raises(ValueError):
+        cpb.classify_field(field, channels=("min", "ridge"))
+    with pytest.raises(ValueError):
+        cpb.classify_field(field, workers=0)
+    with pytest.raises(ValueError):
+        cpb.classify_field(_fit(vals, "gaussian"))
+    with pytest.raises(ValueError):
+        cpb.classify_field(field, cpb.EstimatorSpec(method="semianalytical"))
+    tiny = _fit(np.random.default_rng(0).uniform(0, 1, (4, 2, 3)).astype(np.float32), "uniform")
+    with pytest.raises(ValueError):
+        cpb.classify_field(tiny)
+
+
+def test_workers_do_not_change_results(golden):
+    field = _fit(golden["fit"]["ens/rand"], "histogram", 5)
+    one = cpb.classify_field(field, workers=1)
+    two = cpb.classify_field(field, workers=4)
+    for ch in ("min", "max", "saddle"):
+        assert np.array_equal(one.channel(ch), two.channel(ch))
+
+
+# ---------------------------------------------------------------- Monte Carlo
+def test_monte_carlo_bitexact_against_reference(golden):
+    fit, mc = golden["fit"], golden["mc"]
+    seen = 0
+    for key in mc:
+        parts = key.split("/")
+        if len(parts) != 4 or parts[3] != "n":
+            continue
+        name, kind, bins = parts[0], parts[1], int(parts[2])
+        n = int(mc[key])
+        est = cpb.EstimatorSpec(method="monte_carlo", n_samples=n, seed=9)
+        prob = cpb.classify_field(_fit(fit[f"ens/{name}"], kind, bins), est)
+        for ch in ("min", "max", "saddle"):
+            ref = mc[f"{name}/{kind}/{bins}/{ch}"]
+            got = prob.channel(ch)
+            if kind in ("uniform", "histogram"):
+                assert np.array_equal(got, ref), (name, kind, bins, ch)
+            else:
+                assert np.max(np.abs(got - ref)) <= 1.0 / n + 1e-15, (name, kind, ch)
+        seen += 1
+    assert seen >= 12
+
+
+@pytest.mark.parametrize("kind,bins", [("uniform", 5), ("histogram", 5), ("histogram", 9),
+                                       ("epanechnikov", 5), ("gaussian", 5)])
+def test_monte_carlo_counts_against_oracle(kind, bins):
+    vals = orc.ackley_ensemble(23, 17, 20, noise_amp=0.3, seed=1)
+    n = 3001
+    ref_counts = {}
+    orc.classify(orc.fit(vals, kind, bins), kind, method="monte_carlo", n_samples=n, seed=77,
+                 counts_out=ref_counts)
+    holder = {}
+    cpb.classify_field(_fit(vals, kind, bins),
+                       cpb.EstimatorSpec(method="monte_carlo", n_samples=n, seed=77),
+                       counts_out=holder)
+    got = holder["counts"].cpu().numpy()
+    for i, ch in enumerate(("min", "max", "saddle")):
+        diff = np.abs(got[i] - ref_counts[ch])
+        if kind in ("uniform", "histogram"):
+            assert diff.max() == 0, (kind, ch)
+        else:
+            assert diff.max() <= 1 and diff.sum() <= 3, (kind, ch, diff.max(), diff.sum())
+
+
+def test_monte_carlo_vs_closed_form_binomial_bound():
+    # test_acceptance.py:75-97 style: |p_mc - p_closed| <= 4 SE for >= 99% of vertices
+    vals = orc.ackley_ensemble(64, 64, 20, noise_amp=0.3, seed=0)
+    for kind in ("uniform", "epanechnikov"):
+        field = _fit(vals, kind)
+        closed = cpb.classify_field(field)
+        n = 20000
+        for rng in ("splitmix64", "philox"):
+            mc = cpb.classify_field(field, cpb.EstimatorSpec(method="monte_carlo", n_samples=n,
+                                                             seed=3, rng=rng))
+            for ch in ("min", "max", "saddle"):
+                p = closed.channel(ch)[1:-1, 1:-1]
+                q = mc.channel(ch)[1:-1, 1:-1]
+                se = np.sqrt(np.maximum(p * (1 - p), 1e-12) / n)
+                ok = np.abs(q - p) <= 4 * se + 1e-12
+                assert ok.mean() >= 0.99, (kind, rng, ch, ok.mean())
+
+
+def test_monte_carlo_chunking_boundary(golden):
+    # test_engine.py:642-651: large n, the per-lane split must not matter
+    vals = golden["fit"]["ens/rand"]
+    field = _fit(vals, "uniform")
+    a = cpb.classify_field(field, cpb.EstimatorSpec(method="monte_carlo", n_samples=150_000, seed=3))
+    ref = orc.classify(orc.fit(vals, "uniform"), "uniform", method="monte_carlo", n_samples=150_000,
+                       seed=3, block=8)
+    for ch in ("min", "max", "saddle"):
+        assert np.array_equal(a.channel(ch), ref[ch])
+
+
+# ---------------------------------------------------------------- RNG + synth
+def test_unit_block_bitexact(golden):
+    rng = golden["rng"]
+    for seed in (0, 7, -1, 2**64 - 2, 123456789):
+        assert np.array_equal(cpb.unit_block(seed, rng["pixels"], 3, 11), rng[f"{seed}"])
+    a = cpb.unit_block(5, np.arange(4), 2, 40)
+    assert np.array_equal(a, orc.uniforms(5, np.arange(4), 2, 40))
+
+
+def test_synthetic_rows_match_host_twin():
+    dev = cpb.synthetic_rows(0, 40, 33, 40, 7, seed=4).cpu().numpy()
+    host = orc.synthetic_rows(0, 40, 33, 40, 7, seed=4)
+    assert np.array_equal(dev, host)
+    part = cpb.synthetic_rows(13, 5, 33, 40, 7, seed=4).cpu().numpy()
+    assert np.array_equal(part, host[:, 13:18])
