@@ -97,6 +97,9 @@ typedef struct cpb_field {
   int64_t width;
   int64_t row0;          /* global row index of local row 0 (Monte Carlo pixel keys) */
   int64_t global_width;  /* pixel key = global_row * global_width + col (engine.py:752-754) */
+  int64_t plane_stride;  /* elements between histogram bin planes; 0 = height * width.  Lets a
+                            slab view (offset base pointers, fewer rows) address the bin planes
+                            of a taller allocation, e.g. a row slab with halo rows */
   double eps;            /* from the GLOBAL ensemble range (distributions.py:30-36) */
   double k;              /* epanechnikov k (fields.py:31) */
   void* lo;

@@ -31,6 +31,7 @@ class CpbField(ctypes.Structure):
         ("kind", c_i32), ("bins", c_i32), ("members", c_i32), ("bounds", c_i32),
         ("weights_mode", c_i32), ("reserved", c_i32),
         ("height", c_i64), ("width", c_i64), ("row0", c_i64), ("global_width", c_i64),
+        ("plane_stride", c_i64),
         ("eps", c_dbl), ("k", c_dbl),
         ("lo", c_vp), ("hi", c_vp), ("mean", c_vp), ("spread", c_vp),
         ("weights", c_vp), ("weight_table", c_vp),

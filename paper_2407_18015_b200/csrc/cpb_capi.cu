@@ -299,33 +299,18 @@ int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t wi
     fc.hi = (char*)hi.p + off * (pb[1] ? sizeof(float) : 0);
     fc.mean = pb[2] ? (double*)mean.p + off : nullptr;
     fc.spread = pb[3] ? (double*)spread.p + off : nullptr;
-    fc.weights = wts.p;
-    if (kind == CPB_HISTOGRAM) {
-      // bin planes are (bins, H, W): a chunk view cannot be expressed by a base
-      // pointer alone, so the chunk is fitted into a (bins, nr, W) staging area
-      // and copied into place below
-    }
-    // serialise range accumulation across the two streams via the ring order
+    // bin planes are (bins, H, W): the chunk view offsets the base pointer and
+    // keeps the full-grid plane stride
+    fc.weights = pb[4] ? (char*)wts.p + off * (members <= 255 ? 1 : 2) : nullptr;
+    fc.plane_stride = (int64_t)plane;
+    // range accumulation is serialised across the two streams by the chunk order
     if (nchunks > 0) {
       e = cudaStreamWaitEvent(st, ss.ev[b ^ 1], 0);
       if (e != cudaSuccess) return cuda_status(e, "event wait");
     }
-    if (kind == CPB_HISTOGRAM) {
-      DevBuf stage;
-      const size_t cb = (size_t)nr * width * bins * (members <= 255 ? 1 : 2);
-      if ((s = stage.alloc(cb, st))) return s;
-      fc.weights = stage.p;
-      if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc, (uint32_t*)range.p,
-                       nchunks > 0, st)))
-        return s;
-      const size_t esz = members <= 255 ? 1 : 2;
-      e = cudaMemcpy2DAsync((char*)wts.p + off * esz, plane * esz, stage.p, (size_t)nr * width * esz,
-                            (size_t)nr * width * esz, (size_t)bins, cudaMemcpyDeviceToDevice, st);
-      if (e != cudaSuccess) return cuda_status(e, "histogram plane copy");
-    } else if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc, (uint32_t*)range.p,
-                            nchunks > 0, st))) {
+    if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc, (uint32_t*)range.p,
+                     nchunks > 0, st)))
       return s;
-    }
     f.bounds = fc.bounds;
     f.weights_mode = fc.weights_mode;
     e = cudaEventRecord(ss.ev[b], st);

@@ -181,7 +181,9 @@ CPB_D double pairwise_sum(const Get& get, int n) {
 // ---------------------------------------------------------------------------
 struct FieldView {
   int kind, bins, members, bounds, wmode;
-  int64_t height, width, row0, gwidth, plane;  // plane = height * width
+  int64_t height, width, row0, gwidth;
+  int64_t npix;     // height * width
+  int64_t wstride;  // elements between histogram bin planes
   double eps, k;
   const void* lo;
   const void* hi;
@@ -195,7 +197,9 @@ inline FieldView make_view(const cpb_field& f) {
   FieldView v;
   v.kind = f.kind; v.bins = f.bins; v.members = f.members; v.bounds = f.bounds;
   v.wmode = f.weights_mode; v.height = f.height; v.width = f.width; v.row0 = f.row0;
-  v.gwidth = f.global_width; v.plane = f.height * f.width; v.eps = f.eps; v.k = f.k;
+  v.gwidth = f.global_width; v.npix = f.height * f.width;
+  v.wstride = f.plane_stride > 0 ? f.plane_stride : v.npix;
+  v.eps = f.eps; v.k = f.k;
   v.lo = f.lo; v.hi = f.hi; v.mean = f.mean; v.spread = f.spread; v.weights = f.weights;
   v.wtab = f.weight_table;
   return v;
@@ -242,13 +246,13 @@ CPB_D int degenerate_bin(double c, double lo, double hi, int h) {
 // exact table, the degenerate one-hot, or the stored float64 weight.
 CPB_D double load_weight(const FieldView& v, int64_t idx, int b, bool degenerate, int dbin) {
   if (v.wmode == CPB_WEIGHTS_F64)
-    return __ldg(static_cast<const double*>(v.weights) + (int64_t)b * v.plane + idx);
+    return __ldg(static_cast<const double*>(v.weights) + (int64_t)b * v.wstride + idx);
   if (degenerate) return b == dbin ? 1.0 : 0.0;  // M/M == 1.0 exactly
   unsigned c;
   if (v.wmode == CPB_WEIGHTS_U8)
-    c = __ldg(static_cast<const uint8_t*>(v.weights) + (int64_t)b * v.plane + idx);
+    c = __ldg(static_cast<const uint8_t*>(v.weights) + (int64_t)b * v.wstride + idx);
   else
-    c = __ldg(static_cast<const uint16_t*>(v.weights) + (int64_t)b * v.plane + idx);
+    c = __ldg(static_cast<const uint16_t*>(v.weights) + (int64_t)b * v.wstride + idx);
   return __ldg(v.wtab + c);
 }
 

@@ -23,6 +23,7 @@ struct FitArgs {
   const float* ens;
   int64_t mstride;  // elements between members
   int64_t npix;     // height * width of the slab
+  int64_t wstride;  // elements between bin planes of `counts`
   int members;
   int bins;
   float* lo;
@@ -115,10 +116,10 @@ __global__ void __launch_bounds__(kFitThreads) fit_reg_kernel(FitArgs a) {
       }
       if (a.wmode == CPB_WEIGHTS_U8) {
         uint8_t* c = static_cast<uint8_t*>(a.counts);
-        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint8_t)s_cnt[b * blockDim.x + threadIdx.x];
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.wstride + p] = (uint8_t)s_cnt[b * blockDim.x + threadIdx.x];
       } else {
         uint16_t* c = static_cast<uint16_t*>(a.counts);
-        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint16_t)s_cnt[b * blockDim.x + threadIdx.x];
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.wstride + p] = (uint16_t)s_cnt[b * blockDim.x + threadIdx.x];
       }
     }
     if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) {
@@ -175,10 +176,10 @@ __global__ void __launch_bounds__(kFitThreads) fit_loop_kernel(FitArgs a) {
       }
       if (a.wmode == CPB_WEIGHTS_U8) {
         uint8_t* c = static_cast<uint8_t*>(a.counts);
-        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint8_t)s_cnt[b * blockDim.x + threadIdx.x];
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.wstride + p] = (uint8_t)s_cnt[b * blockDim.x + threadIdx.x];
       } else {
         uint16_t* c = static_cast<uint16_t*>(a.counts);
-        for (int b = 0; b < h; ++b) c[(int64_t)b * a.npix + p] = (uint16_t)s_cnt[b * blockDim.x + threadIdx.x];
+        for (int b = 0; b < h; ++b) c[(int64_t)b * a.wstride + p] = (uint16_t)s_cnt[b * blockDim.x + threadIdx.x];
       }
     }
     if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) {
@@ -221,7 +222,7 @@ __global__ void from_scalar_kernel(const double* v, int64_t n, double half, doub
 // Reference-layout float64 params (fields.py:137-158 outputs).
 __global__ void materialize_kernel(FieldView f, double* a, double* b, double* w) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= f.plane) return;
+  if (p >= f.npix) return;
   if (f.kind == CPB_EPANECHNIKOV) {
     double m, hw;
     load_epan(f, p, m, hw);
@@ -277,6 +278,7 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
   a.ens = ens;
   a.mstride = mstride;
   a.npix = f->height * f->width;
+  a.wstride = f->plane_stride > 0 ? f->plane_stride : a.npix;
   a.members = f->members;
   a.bins = f->bins;
   a.lo = static_cast<float*>(f->lo);
@@ -342,8 +344,8 @@ int launch_from_scalar(const double* v, int64_t n, double half, double* lo, doub
 
 int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cudaStream_t st) {
   const FieldView v = make_view(*f);
-  if (v.plane == 0) return CPB_OK;
-  materialize_kernel<<<grid_for(v.plane, 256), 256, 0, st>>>(v, a, b, w);
+  if (v.npix == 0) return CPB_OK;
+  materialize_kernel<<<grid_for(v.npix, 256), 256, 0, st>>>(v, a, b, w);
   CPB_CHECK_LAUNCH("materialize kernel");
   return CPB_OK;
 }

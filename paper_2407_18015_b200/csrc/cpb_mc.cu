@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a
       if (a.pmax) a.pmax[idx] = __ddiv_rn((double)cmax, n);
       if (a.psad) a.psad[idx] = __ddiv_rn((double)csad, n);
       if (a.counts) {
-        const int64_t plane = f.plane;
+        const int64_t plane = f.npix;
         a.counts[idx] = cmin;
         a.counts[plane + idx] = cmax;
         a.counts[2 * plane + idx] = csad;
