@@ -150,6 +150,7 @@ class KernelTimer:
             self.pending.append((self.kind, what, self.open, ev))
 
     def collect(self):
+        self.torch.cuda.synchronize()
         out = {}
         for kind, what, a, b in self.pending:
             out.setdefault((kind, what), []).append(a.elapsed_time(b))

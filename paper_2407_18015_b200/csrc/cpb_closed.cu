@@ -94,6 +94,24 @@ CPB_D bool vertex(const FieldView& f, const Window& w, int64_t& idx) {
   return true;
 }
 
+// Per-piece state of the neighbour CDFs.  A piece [a, b] of the shared
+// partition lies wholly below, inside or above each neighbour's support (the
+// support ends are partition points), so on that piece the clipped CDF
+// argument of engine.py:518 / 530 is  fma(x - ref, beta, alpha)  with
+// (beta, alpha) = (scale, 0) inside and (0, below | above) outside: one DADD
+// and one FMA per node and neighbour instead of a clip.  The node x itself is
+// rounded exactly like the reference's  mids + halves * xi  (no contraction),
+// so even supports that are tiny next to their offset (degenerate pixels
+// widened by eps) see the same arguments as the reference.
+CPB_D void piece_state(double mid, double lo, double hi, double scale, double below, double above,
+                       double& alpha, double& beta) {
+  const bool inside = mid > lo && mid < hi;
+  alpha = inside ? 0.0 : (mid >= hi ? above : below);
+  beta = inside ? scale : 0.0;
+}
+
+CPB_D double node_x(double mid, double half, double xi) { return __dadd_rn(mid, __dmul_rn(half, xi)); }
+
 // ----------------------------------------------------------------- uniform
 // pdf_C = 1/(hi_C - lo_C); F_P(x) = clip((x - lo_P)/(hi_P - lo_P), 0, 1)
 // (engine.py:510-520), 3-node Gauss-Legendre per piece (integrand degree 4).
@@ -123,20 +141,23 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
     const double b = i < 8 ? k[i] : hi[C_];
     if (b > a) {
       const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+      double al[5], be[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) piece_state(mid, lo[p], hi[p], inv[p], 0.0, 1.0, al[p], be[p]);
       double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int j = 0; j < GL3::n; ++j) {
-        const double x = mid + half * GL3::x(j);
+        const double x = node_x(mid, half, GL3::x(j));
         double F[5], g[4];
 #pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = clamp01((x - lo[p]) * inv[p]);
+        for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
         integrands(F, g);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] += GL3::w(j) * g[r];
+        for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (a >= rg.lo[r] && b <= rg.hi[r]) acc[r] += s[r] * half;
+        if (a >= rg.lo[r] && b <= rg.hi[r]) acc[r] = fma(s[r], half, acc[r]);
     }
     a = dmax(a, b);
   }
@@ -148,6 +169,10 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
 // ------------------------------------------------------------ epanechnikov
 // pdf_C = 0.75/hw_C (1 - u^2), u unclipped; F_P = 0.5 + 0.75u - 0.25u^3 with
 // u clipped to [-1, 1] (engine.py:521-533); 8-node Gauss-Legendre (degree 14).
+// Outside a neighbour's support the affine form pins u to -1 or +1, where the
+// cubic gives exactly 0 or 1, so no clip is evaluated per node.
+CPB_D double epan_cdf(double u) { return fma(u, fma(-0.25, u * u, 0.75), 0.5); }
+
 __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
     FieldView f, Window w, double* pmin, double* pmax, double* psad) {
   int64_t idx;
@@ -173,30 +198,33 @@ __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
   merge_pairs8(k);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   double a = lo[C_];
-#pragma unroll
+#pragma unroll 1
   for (int i = 0; i < 9; ++i) {
-    const double b = i < 8 ? k[i] : hi[C_];
+    double b = hi[C_];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q == i) b = k[q];
     if (b > a) {
       const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+      double al[5], be[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) piece_state(mid, lo[p], hi[p], ih[p], -1.0, 1.0, al[p], be[p]);
       double s[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int j = 0; j < GL8::n; ++j) {
-        const double x = mid + half * GL8::x(j);
+        const double x = node_x(mid, half, GL8::x(j));
         const double uc = (x - m[C_]) * ih[C_];
-        const double wp = GL8::w(j) * (pdf0 * (1.0 - uc * uc));
+        const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
         double F[5], g[4];
 #pragma unroll
-        for (int p = 1; p < 5; ++p) {
-          const double u = dmin(dmax((x - m[p]) * ih[p], -1.0), 1.0);
-          F[p] = 0.5 + u * (0.75 - 0.25 * (u * u));
-        }
+        for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
         integrands(F, g);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] += wp * g[r];
+        for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
       }
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        if (a >= rg.lo[r] && b <= rg.hi[r]) acc[r] += s[r] * half;
+        if (a >= rg.lo[r] && b <= rg.hi[r]) acc[r] = fma(s[r], half, acc[r]);
     }
     a = dmax(a, b);
   }
@@ -251,7 +279,9 @@ CPB_D void enter_bin(const FieldView& f, const HistPos& P, Sweep& st, int h) {
   st.next = edge_at(P, st.j + 1, h);
 }
 
-__global__ void __launch_bounds__(kClosedThreads) closed_hist_kernel(
+// Fallback for very many bins (> kHistSmemMaxBins): per-thread state, weights
+// read from global memory.
+__global__ void __launch_bounds__(kClosedThreads) closed_hist_global_kernel(
     FieldView f, Window w, double* pmin, double* pmax, double* psad) {
   int64_t idx;
   if (!vertex(f, w, idx)) return;
@@ -327,6 +357,144 @@ __global__ void __launch_bounds__(kClosedThreads) closed_hist_kernel(
   store(pmin, pmax, psad, idx, acc);
 }
 
+// Shared-memory histogram stencil (the production path for bins <= 64).
+// A block of TW threads computes TW consecutive vertices of one row.  First the
+// block stages the 3 x (TW + 2) pixels the stencil touches: support bounds,
+// bin widths and the renormalised weights wn = w / sum(w) (numpy pairwise
+// order for the sum), all in float64 shared memory; then every thread sweeps
+// its five edge lists reading only shared memory.
+constexpr int kHistSmemMaxBins = 64;
+
+struct HistTile {
+  int sw;            // staged row width = TW + 2
+  double* lo;        // [3 * sw]
+  double* hi;
+  double* width;     // hi - lo
+  double* binw;
+  double* ibinw;
+  double* wn;        // [bins][3 * sw]
+  double* kh;        // k / h for k = 0..h
+};
+
+struct NState {      // one neighbour inside the current piece: F(x) = c + s (x - e)
+  int j;
+  double next, cum, wj, c, s, e;
+};
+
+CPB_D void nb_enter(const HistTile& T, int i, int h, double hi, NState& st) {
+  if (st.j >= 0) st.cum += st.wj;  // np.cumsum order
+  st.j += 1;
+  if (st.j >= h) {
+    st.c = 1.0; st.s = 0.0; st.e = 0.0; st.wj = 0.0;
+    st.next = __longlong_as_double(0x7ff0000000000000ll);
+    return;
+  }
+  const int n = 3 * T.sw;
+  st.wj = T.wn[st.j * n + i];
+  st.c = st.cum;
+  st.s = st.wj * T.ibinw[i];
+  st.e = T.lo[i] + T.binw[i] * (double)st.j;
+  st.next = st.j + 1 >= h ? hi : T.lo[i] + T.width[i] * T.kh[st.j + 1];
+}
+
+__global__ void closed_hist_smem_kernel(FieldView f, Window w, double* pmin, double* pmax,
+                                        double* psad) {
+  extern __shared__ double sm[];
+  const int TW = blockDim.x, sw = TW + 2, n = 3 * sw, h = f.bins;
+  HistTile T;
+  T.sw = sw;
+  T.lo = sm;
+  T.hi = sm + n;
+  T.width = sm + 2 * n;
+  T.binw = sm + 3 * n;
+  T.ibinw = sm + 4 * n;
+  T.wn = sm + 5 * n;
+  T.kh = T.wn + (size_t)h * n;
+  const int64_t tile = blockIdx.x % w.ntiles;
+  const int64_t r = w.row_begin + blockIdx.x / w.ntiles;
+  const int64_t c0 = tile * TW;  // staged columns [c0, c0 + sw)
+  for (int k = threadIdx.x; k <= h; k += TW) T.kh[k] = (double)k / (double)h;
+  for (int i = threadIdx.x; i < n; i += TW) {
+    const int64_t rr = r - 1 + i / sw, cc = c0 + i % sw;
+    if (cc >= f.width) continue;
+    const int64_t at = rr * f.width + cc;
+    double lo, hi;
+    const bool deg = load_bounds(f, at, lo, hi);
+    const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at), lo, hi, h) : 0;
+    for (int b = 0; b < h; ++b) T.wn[b * n + i] = load_weight(f, at, b, deg, dbin);
+    const double total = pairwise_sum([&](int b) { return T.wn[b * n + i]; }, h);
+    const double it = 1.0 / total;
+    for (int b = 0; b < h; ++b) T.wn[b * n + i] *= it;
+    T.lo[i] = lo;
+    T.hi[i] = hi;
+    T.width[i] = hi - lo;
+    T.binw[i] = (hi - lo) / (double)h;
+    T.ibinw[i] = 1.0 / T.binw[i];
+  }
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int64_t c = c0 + 1 + t;
+  if (c >= f.width - 1) return;
+  const int64_t idx = r * f.width + c;
+  const int li[5] = {sw + t + 1, sw + t + 2, t + 1, sw + t, 2 * sw + t + 1};  // C E N W S
+  double lo[5], hi[5];
+#pragma unroll
+  for (int p = 0; p < 5; ++p) {
+    lo[p] = T.lo[li[p]];
+    hi[p] = T.hi[li[p]];
+  }
+  const Ranges rg = make_ranges(lo, hi);
+  const double x0 = lo[C_], xend = hi[C_];
+  NState st[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    st[p].j = -1; st[p].cum = 0.0; st[p].wj = 0.0; st[p].c = 0.0; st[p].s = 0.0; st[p].e = 0.0;
+    st[p].next = lo[p];
+    while (st[p].next <= x0) nb_enter(T, li[p], h, hi[p], st[p]);
+  }
+  const int ic = li[C_];
+  int jc = 0;
+  double pdf = T.wn[ic] * T.ibinw[ic];
+  double nextc = h > 1 ? T.lo[ic] + T.width[ic] * T.kh[1] : xend;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double x = x0;
+  while (x < xend) {
+    const double xn = dmin(dmin(nextc, dmin(st[E_].next, st[N_].next)), dmin(st[W_].next, st[S_].next));
+    if (xn > x) {
+      const double half = 0.5 * (xn - x), mid = 0.5 * (xn + x);
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int j = 0; j < GL3::n; ++j) {
+        const double xx = node_x(mid, half, GL3::x(j));
+        double F[5], g[4];
+#pragma unroll
+        for (int p = 1; p < 5; ++p) F[p] = fma(xx - st[p].e, st[p].s, st[p].c);
+        integrands(F, g);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(j), g[q], s[q]);
+      }
+      const double scale = pdf * half;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (x >= rg.lo[q] && xn <= rg.hi[q]) acc[q] = fma(s[q], scale, acc[q]);
+    }
+    if (nextc == xn) {
+      ++jc;
+      if (jc >= h) {
+        nextc = __longlong_as_double(0x7ff0000000000000ll);
+      } else {
+        pdf = T.wn[jc * n + ic] * T.ibinw[ic];
+        nextc = jc + 1 >= h ? xend : T.lo[ic] + T.width[ic] * T.kh[jc + 1];
+      }
+    }
+#pragma unroll
+    for (int p = 1; p < 5; ++p)
+      if (st[p].next == xn) nb_enter(T, li[p], h, hi[p], st[p]);
+    x = dmax(x, xn);
+  }
+  store(pmin, pmax, psad, idx, acc);
+}
+
 }  // namespace
 
 int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
@@ -349,9 +517,23 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     case CPB_EPANECHNIKOV:
       closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
       break;
-    case CPB_HISTOGRAM:
-      closed_hist_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+    case CPB_HISTOGRAM: {
+      if (f.bins > kHistSmemMaxBins) {
+        closed_hist_global_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+        break;
+      }
+      // tile width so the staged float64 weights fit comfortably in shared memory
+      int tw = 128;
+      while (tw > 32 && (size_t)(5 + f.bins) * 3 * (tw + 2) * 8 > 64 * 1024) tw >>= 1;
+      Window wh = w;
+      wh.ntiles = (int)((f.width - 2 + tw - 1) / tw);
+      const int64_t hb = rows * wh.ntiles;
+      const size_t smem = ((size_t)(5 + f.bins) * 3 * (tw + 2) + f.bins + 1) * 8;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(closed_hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      closed_hist_smem_kernel<<<(unsigned)hb, tw, smem, st>>>(f, wh, pmin, pmax, psad);
       break;
+    }
     default:
       set_error("Gaussian fields have no closed form; use monte_carlo");
       return CPB_EINVAL;

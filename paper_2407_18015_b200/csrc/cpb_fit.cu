@@ -12,6 +12,9 @@
 #include <algorithm>
 
 #include "cpb_common.cuh"
+#include "cpb_tma.cuh"
+
+#include <cudaTypedefs.h>
 
 namespace cpb {
 namespace {
@@ -196,6 +199,163 @@ __global__ void __launch_bounds__(kFitThreads) fit_loop_kernel(FitArgs a) {
   merge_range(vmin, vmax, bad, a.range);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-pipelined fit: the production path.
+//
+// A persistent CTA of kTmaTile threads owns one pixel per thread of a tile of
+// kTmaTile consecutive pixels.  The tile's M member rows form one 2-D box of
+// the (members x pixels) tensor view of the ensemble; one TMA instruction
+// (cp.async.bulk.tensor.2d, completion on an mbarrier) stages it into shared
+// memory through a ring of `stages` buffers, so several tiles per SM are in
+// flight while the threads reduce the staged one.  Both passes of the
+// two-pass statistics (mean then squared deviations; min/max then bin counts)
+// read the staged values, so HBM sees every member value exactly once.
+// ---------------------------------------------------------------------------
+constexpr int kTmaTile = 128;
+constexpr int kThreshBins = 8;  // histogram bins counted with per-thread thresholds
+
+// Smallest float v with floor(fl(fl(v - lo) * scale)) >= k -- the bin index of
+// fields.py:147 is monotone in v, so "bin >= k" is "v >= threshold_k" and the
+// per-member binning becomes h-1 float compares, bit-exact by construction.
+CPB_D float bin_threshold(int k, double lo, double scale) {
+  auto raw = [&](float v) { return floor(__dmul_rn(__dsub_rn((double)v, lo), scale)); };
+  float c = __double2float_rn(__dadd_rn(lo, __ddiv_rn((double)k, scale)));
+  const double kk = (double)k;
+  if (raw(c) >= kk) {
+    for (int it = 0; it < 64; ++it) {
+      const float d = nextafterf(c, -__int_as_float(0x7f800000));
+      if (raw(d) >= kk) c = d; else break;
+    }
+  } else {
+    for (int it = 0; it < 64 && raw(c) < kk; ++it) c = nextafterf(c, __int_as_float(0x7f800000));
+  }
+  return c;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant__ CUtensorMap map,
+                                                           FitArgs a, int stages, int mbox,
+                                                           int nbox, int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int M = a.members;
+  const int rows = mbox * nbox;  // staged member rows per tile (>= M, OOB rows are zero)
+  const int tid = threadIdx.x;
+  float* buf = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * rows * kTmaTile * 4);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(full + stages);  // (bins, kTmaTile), bins > kThreshBins
+  if (tid == 0) {
+    prefetch_tensormap(&map);
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const uint32_t tile_bytes = (uint32_t)rows * kTmaTile * 4u;
+  auto issue = [&](int64_t tile, int s) {  // one thread
+    mbar_arrive_expect_tx(&full[s], tile_bytes);
+    float* dst = buf + (size_t)s * rows * kTmaTile;
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(dst + (size_t)b * mbox * kTmaTile, &map, (int)(tile * kTmaTile), b * mbox, &full[s], pol);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < stages; ++k) {
+      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+      if (t < ntiles) issue(t, k);
+    }
+  }
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % stages;
+    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+    const float* col = buf + (size_t)s * rows * kTmaTile + tid;
+    const int64_t p = t * kTmaTile + tid;
+    if (p < a.npix) {
+      float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+      double sum = 0.0;
+#pragma unroll 8
+      for (int m = 0; m < M; ++m) {
+        const float x = col[m * kTmaTile];
+        bad |= nonfinite(x);
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+        if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) sum = __dadd_rn(sum, (double)x);
+      }
+      vmin = fminf(vmin, lo);
+      vmax = fmaxf(vmax, hi);
+      if (KIND == CPB_UNIFORM || KIND == CPB_HISTOGRAM) {
+        a.lo[p] = lo;
+        a.hi[p] = hi;
+      }
+      if (KIND == CPB_HISTOGRAM) {
+        const int h = a.bins;
+        const double dlo = (double)lo;
+        const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
+        uint32_t c[kThreshBins + 1];
+        if (h <= kThreshBins) {
+          // cumulative counts C_k = #{v >= thr_k}; bin b holds C_b - C_{b+1}
+          float thr[kThreshBins];
+#pragma unroll
+          for (int q = 1; q < kThreshBins; ++q)
+            thr[q] = (q < h && hi > lo) ? bin_threshold(q, dlo, scale) : __int_as_float(0x7f800000);
+#pragma unroll
+          for (int q = 0; q <= kThreshBins; ++q) c[q] = 0u;
+#pragma unroll 4
+          for (int m = 0; m < M; ++m) {
+            const float x = col[m * kTmaTile];
+#pragma unroll
+            for (int q = 1; q < kThreshBins; ++q) c[q] += (x >= thr[q]) ? 1u : 0u;
+          }
+          c[0] = (uint32_t)M;
+        } else {
+          for (int b = 0; b < h; ++b) cnt[b * kTmaTile + tid] = 0u;
+          if (hi > lo)
+            for (int m = 0; m < M; ++m) cnt[bin_of(col[m * kTmaTile], dlo, scale, h) * kTmaTile + tid] += 1u;
+        }
+        const bool flat = !(hi > lo);  // degenerate: counts resolved at use, once eps is known
+        auto count = [&](int b) -> uint32_t {
+          if (flat) return 0u;
+          if (h <= kThreshBins) {
+            uint32_t cb = 0u, cn = 0u;
+#pragma unroll
+            for (int q = 0; q <= kThreshBins; ++q) {
+              if (q == b) cb = c[q];
+              if (q == b + 1) cn = c[q];
+            }
+            return b + 1 >= h ? cb : cb - cn;
+          }
+          return cnt[b * kTmaTile + tid];
+        };
+        if (a.wmode == CPB_WEIGHTS_U8) {
+          uint8_t* dst = static_cast<uint8_t*>(a.counts);
+          for (int b = 0; b < h; ++b) dst[(int64_t)b * a.wstride + p] = (uint8_t)count(b);
+        } else {
+          uint16_t* dst = static_cast<uint16_t*>(a.counts);
+          for (int b = 0; b < h; ++b) dst[(int64_t)b * a.wstride + p] = (uint16_t)count(b);
+        }
+      }
+      if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) {
+        const double mean = __ddiv_rn(sum, (double)M);
+        double sq = 0.0;
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const double d = __dsub_rn((double)col[m * kTmaTile], mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+        a.mean[p] = mean;
+        a.spread[p] = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)stages * gridDim.x;
+      if (tn < ntiles) issue(tn, s);
+    }
+  }
+  merge_range(vmin, vmax, bad, a.range);
+}
+
 __global__ void range_init_kernel(uint32_t* range) {
   range[0] = 0xffffffffu;
   range[1] = 0u;
@@ -268,6 +428,30 @@ __global__ void synth_kernel(float* ens, int64_t mstride, int members, int64_t r
   }
 }
 
+}  // namespace
+
+bool encode_tensor_map_2d_f32(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1,
+                              uint64_t stride1_bytes, uint32_t box0, uint32_t box1) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !ptr)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1_bytes};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
+
 inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + threads - 1) / threads); }
 
 }  // namespace
@@ -298,6 +482,63 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
   if (f->kind == CPB_HISTOGRAM) {
     weight_table_kernel<<<grid_for(f->members + 1, 256), 256, 0, st>>>(f->weight_table, f->members);
     CPB_CHECK_LAUNCH("weight table");
+  }
+  // production path: TMA-staged tiles (member stride must be a multiple of 16 bytes)
+  const int mbox = std::min(f->members, 256);
+  const int nbox = (f->members + mbox - 1) / mbox;
+  const size_t tile_bytes = (size_t)mbox * nbox * kTmaTile * 4;
+  const size_t cnt_bytes =
+      (f->kind == CPB_HISTOGRAM && f->bins > kThreshBins) ? (size_t)f->bins * kTmaTile * 4 : 0;
+  const bool tma_ok = (mstride % 4 == 0) && ((reinterpret_cast<uintptr_t>(ens) & 15) == 0) &&
+                      tile_bytes * 2 + cnt_bytes + 64 <= 200 * 1024;
+  if (tma_ok) {
+    const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, (96 * 1024) / tile_bytes));
+    const size_t smem = stages * tile_bytes + stages * 8 + cnt_bytes;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // TMA coordinates are int32: split very large slabs into pixel chunks
+    const int64_t max_chunk = (int64_t)1 << 30;
+    for (int64_t p0 = 0; p0 < a.npix; p0 += max_chunk) {
+      FitArgs c = a;
+      const int64_t n = std::min(max_chunk, a.npix - p0);
+      c.ens = ens + p0;
+      c.npix = n;
+      c.lo = a.lo ? a.lo + p0 : nullptr;
+      c.hi = a.hi ? a.hi + p0 : nullptr;
+      c.mean = a.mean ? a.mean + p0 : nullptr;
+      c.spread = a.spread ? a.spread + p0 : nullptr;
+      c.counts = a.counts ? static_cast<char*>(a.counts) + p0 * (a.wmode == CPB_WEIGHTS_U8 ? 1 : 2) : nullptr;
+      CUtensorMap map;
+      if (!encode_tensor_map_2d_f32(&map, c.ens, (uint64_t)n, (uint64_t)f->members,
+                                    (uint64_t)mstride * 4, kTmaTile, (uint32_t)mbox)) {
+        set_error("cuTensorMapEncodeTiled failed");
+        return CPB_ECUDA;
+      }
+      const int64_t ntiles = (n + kTmaTile - 1) / kTmaTile;
+#define CPB_FIT_TMA(K)                                                                           \
+  case K: {                                                                                      \
+    auto kern = fit_tma_kernel<K>;                                                               \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
+    int per_sm = 1;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaTile, smem);                \
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
+    kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);            \
+    break;                                                                                       \
+  }
+      switch (f->kind) {
+        CPB_FIT_TMA(CPB_UNIFORM)
+        CPB_FIT_TMA(CPB_EPANECHNIKOV)
+        CPB_FIT_TMA(CPB_HISTOGRAM)
+        CPB_FIT_TMA(CPB_GAUSSIAN)
+        default:
+          set_error("unknown model kind %d", f->kind);
+          return CPB_EINVAL;
+      }
+#undef CPB_FIT_TMA
+      CPB_CHECK_LAUNCH("fit kernel (TMA)");
+    }
+    return CPB_OK;
   }
   int threads = kFitThreads;
   size_t smem = 0;
