@@ -16,6 +16,8 @@
 //
 // Arithmetic is float64 throughout (closed-form parity bar: 1e-12 absolute,
 // the reference's own grid-vs-case tolerance, test_engine.py:548-559).
+#include <stdlib.h>
+
 #include "cpb_common.cuh"
 
 namespace cpb {
@@ -97,36 +99,124 @@ CPB_D bool vertex(const FieldView& f, const Window& w, int64_t& idx) {
 // Per-piece state of the neighbour CDFs.  A piece [a, b] of the shared
 // partition lies wholly below, inside or above each neighbour's support (the
 // support ends are partition points), so on that piece the clipped CDF
-// argument of engine.py:518 / 530 is  fma(x - ref, beta, alpha)  with
-// (beta, alpha) = (scale, 0) inside and (0, below | above) outside: one DADD
-// and one FMA per node and neighbour instead of a clip.  The node x itself is
-// rounded exactly like the reference's  mids + halves * xi  (no contraction),
-// so even supports that are tiny next to their offset (degenerate pixels
-// widened by eps) see the same arguments as the reference.
-CPB_D void piece_state(double mid, double lo, double hi, double scale, double below, double above,
-                       double& alpha, double& beta) {
-  const bool inside = mid > lo && mid < hi;
-  alpha = inside ? 0.0 : (mid >= hi ? above : below);
-  beta = inside ? scale : 0.0;
+// argument of engine.py:518 / 530 is affine in x:  fma(x - ref, beta, alpha)
+// with (beta, alpha) = (scale, 0) inside and (0, below | above) outside --
+// no clip per node.  The same below/above flags give each piece's membership
+// in the four integration ranges (range_masks).
+//
+// Two evaluation modes per vertex:
+//  - exact: every node x is rounded like the reference's  mids + halves * xi
+//    (no contraction) before the subtraction, so supports that are tiny next
+//    to their offset (eps-widened degenerate pixels) see the reference's
+//    arguments bit for bit;
+//  - fast (|x| / support width <= kFastRatio at all five positions): the
+//    CDF is evaluated at the piece midpoint and moved to the symmetric nodes
+//    mid +- tau along its slope, which skips the per-node x rounding; the
+//    difference to the reference is <= ulp(x) / width * kFastRatio-bounded,
+//    i.e. < 3e-14 in every probability (tolerance 1e-12).
+constexpr double kFastRatio = 256.0;
+
+CPB_D void piece_flags(double mid, double lo, double hi, bool& below, bool& above) {
+  above = mid >= hi;
+  below = mid <= lo;
+}
+
+// Which of the four integrals a piece belongs to, from the neighbour states
+// alone: the ranges of engine.py:603-628 start at max(lo) / end at min(hi) of
+// some positions, and a position's lo / hi are its first / last partition
+// edge, so "piece right of lo_P" is "P not below" and "piece left of hi_P" is
+// "P not above".  (min: nobody above; max: nobody below; t1: N, S not below
+// and E, W not above; t2: E, W not below and N, S not above.)
+CPB_D void range_masks(bool bE, bool bN, bool bW, bool bS, bool aE, bool aN, bool aW, bool aS,
+                       bool m[4]) {
+  m[0] = !(aE | aN | aW | aS);
+  m[1] = !(bE | bN | bW | bS);
+  m[2] = !(bN | bS | aE | aW);
+  m[3] = !(bE | bW | aN | aS);
 }
 
 CPB_D double node_x(double mid, double half, double xi) { return __dadd_rn(mid, __dmul_rn(half, xi)); }
 
+CPB_D double piece_end(const double* k, double hiC, int i) {
+  double b = hiC;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (q == i) b = k[q];
+  return b;
+}
+
 // ----------------------------------------------------------------- uniform
 // pdf_C = 1/(hi_C - lo_C); F_P(x) = clip((x - lo_P)/(hi_P - lo_P), 0, 1)
 // (engine.py:510-520), 3-node Gauss-Legendre per piece (integrand degree 4).
+template <bool FAST>
+CPB_D void uniform_pieces(const double* lo, const double* hi, const double* inv, const double* k,
+                          double acc[4]) {
+  double a = lo[C_];
+#pragma unroll 1
+  for (int i = 0; i < 9; ++i) {
+    const double b = piece_end(k, hi[C_], i);
+    if (b > a) {
+      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+      bool bl[5], ab[5];
+      double al[5], be[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
+        const bool in = !(bl[p] | ab[p]);
+        be[p] = in ? inv[p] : 0.0;
+        al[p] = in ? (FAST ? (mid - lo[p]) * inv[p] : 0.0) : (ab[p] ? 1.0 : 0.0);
+      }
+      double s[4], F[5], g[4];
+      if (FAST) {
+        const double tau = half * GL3::x(2);
+#pragma unroll
+        for (int p = 1; p < 5; ++p) F[p] = al[p];
+        integrands(F, g);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s[r] = GL3::w(1) * g[r];
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+#pragma unroll
+          for (int p = 1; p < 5; ++p) F[p] = fma(side ? tau : -tau, be[p], al[p]);
+          integrands(F, g);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(0), g[r], s[r]);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s[r] = 0.0;
+#pragma unroll
+        for (int j = 0; j < GL3::n; ++j) {
+          const double x = node_x(mid, half, GL3::x(j));
+#pragma unroll
+          for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
+          integrands(F, g);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
+        }
+      }
+      bool m[4];
+      range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], m);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = m[r] ? fma(s[r], half, acc[r]) : acc[r];
+    }
+    a = dmax(a, b);
+  }
+}
+
 __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
     FieldView f, Window w, double* pmin, double* pmax, double* psad) {
   int64_t idx;
   if (!vertex(f, w, idx)) return;
   const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
   double lo[5], hi[5], inv[5];
+  bool fast = true;
 #pragma unroll
   for (int p = 0; p < 5; ++p) {
     load_bounds(f, at[p], lo[p], hi[p]);
     inv[p] = 1.0 / (hi[p] - lo[p]);
+    fast &= (fabs(lo[p]) + fabs(hi[p])) * inv[p] <= kFastRatio;
   }
-  const Ranges rg = make_ranges(lo, hi);
   double k[8];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
@@ -135,32 +225,8 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
   }
   merge_pairs8(k);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  double a = lo[C_];
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    const double b = i < 8 ? k[i] : hi[C_];
-    if (b > a) {
-      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-      double al[5], be[5];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) piece_state(mid, lo[p], hi[p], inv[p], 0.0, 1.0, al[p], be[p]);
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < GL3::n; ++j) {
-        const double x = node_x(mid, half, GL3::x(j));
-        double F[5], g[4];
-#pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
-        integrands(F, g);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (a >= rg.lo[r] && b <= rg.hi[r]) acc[r] = fma(s[r], half, acc[r]);
-    }
-    a = dmax(a, b);
-  }
+  if (fast) uniform_pieces<true>(lo, hi, inv, k, acc);
+  else uniform_pieces<false>(lo, hi, inv, k, acc);
 #pragma unroll
   for (int r = 0; r < 4; ++r) acc[r] *= inv[C_];
   store(pmin, pmax, psad, idx, acc);
@@ -170,8 +236,69 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
 // pdf_C = 0.75/hw_C (1 - u^2), u unclipped; F_P = 0.5 + 0.75u - 0.25u^3 with
 // u clipped to [-1, 1] (engine.py:521-533); 8-node Gauss-Legendre (degree 14).
 // Outside a neighbour's support the affine form pins u to -1 or +1, where the
-// cubic gives exactly 0 or 1, so no clip is evaluated per node.
+// cubic gives exactly 0 or 1.
 CPB_D double epan_cdf(double u) { return fma(u, fma(-0.25, u * u, 0.75), 0.5); }
+
+template <bool FAST>
+CPB_D void epan_pieces(const double* m, const double* ih, const double* lo, const double* hi,
+                       const double* k, double acc[4]) {
+  const double pdf0 = 0.75 * ih[C_];
+  double a = lo[C_];
+#pragma unroll 1
+  for (int i = 0; i < 9; ++i) {
+    const double b = piece_end(k, hi[C_], i);
+    if (b > a) {
+      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+      bool bl[5], ab[5];
+      double al[5], be[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
+        const bool in = !(bl[p] | ab[p]);
+        be[p] = in ? ih[p] : 0.0;
+        al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (ab[p] ? 1.0 : -1.0);
+      }
+      const double uc0 = (mid - m[C_]) * ih[C_];
+      double s[4] = {0.0, 0.0, 0.0, 0.0};
+      if (FAST) {
+#pragma unroll
+        for (int j = 0; j < GL8::n / 2; ++j) {
+          const double tau = half * GL8::x(7 - j);
+#pragma unroll
+          for (int side = 0; side < 2; ++side) {
+            const double t = side ? tau : -tau;
+            const double uc = fma(t, ih[C_], uc0);
+            const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+            double F[5], g[4];
+#pragma unroll
+            for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
+            integrands(F, g);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < GL8::n; ++j) {
+          const double x = node_x(mid, half, GL8::x(j));
+          const double uc = (x - m[C_]) * ih[C_];
+          const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+          double F[5], g[4];
+#pragma unroll
+          for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
+          integrands(F, g);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+        }
+      }
+      bool mk[4];
+      range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = mk[r] ? fma(s[r], half, acc[r]) : acc[r];
+    }
+    a = dmax(a, b);
+  }
+}
 
 __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
     FieldView f, Window w, double* pmin, double* pmax, double* psad) {
@@ -179,6 +306,7 @@ __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
   if (!vertex(f, w, idx)) return;
   const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
   double m[5], ih[5], lo[5], hi[5];
+  bool fast = true;
 #pragma unroll
   for (int p = 0; p < 5; ++p) {
     double hw;
@@ -186,9 +314,8 @@ __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
     ih[p] = 1.0 / hw;
     lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
     hi[p] = m[p] + hw;
+    fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
   }
-  const double pdf0 = 0.75 * ih[C_];
-  const Ranges rg = make_ranges(lo, hi);
   double k[8];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
@@ -197,37 +324,8 @@ __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
   }
   merge_pairs8(k);
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  double a = lo[C_];
-#pragma unroll 1
-  for (int i = 0; i < 9; ++i) {
-    double b = hi[C_];
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q == i) b = k[q];
-    if (b > a) {
-      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-      double al[5], be[5];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) piece_state(mid, lo[p], hi[p], ih[p], -1.0, 1.0, al[p], be[p]);
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-      for (int j = 0; j < GL8::n; ++j) {
-        const double x = node_x(mid, half, GL8::x(j));
-        const double uc = (x - m[C_]) * ih[C_];
-        const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-        double F[5], g[4];
-#pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
-        integrands(F, g);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (a >= rg.lo[r] && b <= rg.hi[r]) acc[r] = fma(s[r], half, acc[r]);
-    }
-    a = dmax(a, b);
-  }
+  if (fast) epan_pieces<true>(m, ih, lo, hi, k, acc);
+  else epan_pieces<false>(m, ih, lo, hi, k, acc);
   store(pmin, pmax, psad, idx, acc);
 }
 
@@ -359,61 +457,37 @@ __global__ void __launch_bounds__(kClosedThreads) closed_hist_global_kernel(
 
 // Shared-memory histogram stencil (the production path for bins <= 64).
 // A block of TW threads computes TW consecutive vertices of one row.  First the
-// block stages the 3 x (TW + 2) pixels the stencil touches: support bounds,
-// bin widths and the renormalised weights wn = w / sum(w) (numpy pairwise
-// order for the sum), all in float64 shared memory; then every thread sweeps
-// its five edge lists reading only shared memory.
+// block stages the 3 x (TW + 2) pixels the stencil touches -- support bounds
+// and the renormalised weights wn = w / sum(w) (numpy pairwise order for the
+// sum) -- in float64 shared memory; then every thread sweeps its five sorted
+// edge lists in merge order (the partition of engine.py:580-582 without a
+// sort), carrying each neighbour's current bin and running prefix sum
+// (np.cumsum order) from piece to piece.  The per-edge advance is written as
+// selects, not branches, so lanes advancing different neighbours never
+// diverge.
 constexpr int kHistSmemMaxBins = 64;
+constexpr int kHistThreads = 128;
 
-struct HistTile {
-  int sw;            // staged row width = TW + 2
-  double* lo;        // [3 * sw]
-  double* hi;
-  double* width;     // hi - lo
-  double* binw;
-  double* ibinw;
-  double* wn;        // [bins][3 * sw]
-  double* kh;        // k / h for k = 0..h
+struct Nb {          // one neighbour: constants + state inside the current piece
+  double lo, width, binw;
+  int i;             // staged pixel index
+  int j;             // current bin; -1 below the support, h above it
+  double next;       // next edge strictly ahead (+inf when none)
+  double c, s, e;    // F(x) = c + s (x - e); c = prefix sum of wn below bin j
 };
 
-struct NState {      // one neighbour inside the current piece: F(x) = c + s (x - e)
-  int j;
-  double next, cum, wj, c, s, e;
-};
-
-CPB_D void nb_enter(const HistTile& T, int i, int h, double hi, NState& st) {
-  if (st.j >= 0) st.cum += st.wj;  // np.cumsum order
-  st.j += 1;
-  if (st.j >= h) {
-    st.c = 1.0; st.s = 0.0; st.e = 0.0; st.wj = 0.0;
-    st.next = __longlong_as_double(0x7ff0000000000000ll);
-    return;
-  }
-  const int n = 3 * T.sw;
-  st.wj = T.wn[st.j * n + i];
-  st.c = st.cum;
-  st.s = st.wj * T.ibinw[i];
-  st.e = T.lo[i] + T.binw[i] * (double)st.j;
-  st.next = st.j + 1 >= h ? hi : T.lo[i] + T.width[i] * T.kh[st.j + 1];
-}
-
-__global__ void closed_hist_smem_kernel(FieldView f, Window w, double* pmin, double* pmax,
-                                        double* psad) {
+template <int MINB>
+__global__ void __launch_bounds__(kHistThreads, MINB) closed_hist_smem_kernel(
+    FieldView f, Window w, double* pmin, double* pmax, double* psad) {
   extern __shared__ double sm[];
   const int TW = blockDim.x, sw = TW + 2, n = 3 * sw, h = f.bins;
-  HistTile T;
-  T.sw = sw;
-  T.lo = sm;
-  T.hi = sm + n;
-  T.width = sm + 2 * n;
-  T.binw = sm + 3 * n;
-  T.ibinw = sm + 4 * n;
-  T.wn = sm + 5 * n;
-  T.kh = T.wn + (size_t)h * n;
+  // layout: lo[n] hi[n] ibinw[n] wn[h][n] kh[h+1]
+  const int o_hi = n, o_ib = 2 * n, o_wn = 3 * n, o_kh = (3 + h) * n;
   const int64_t tile = blockIdx.x % w.ntiles;
   const int64_t r = w.row_begin + blockIdx.x / w.ntiles;
   const int64_t c0 = tile * TW;  // staged columns [c0, c0 + sw)
-  for (int k = threadIdx.x; k <= h; k += TW) T.kh[k] = (double)k / (double)h;
+  for (int k = threadIdx.x; k <= h; k += TW) sm[o_kh + k] = (double)k / (double)h;
+  const double invM = 1.0 / (double)f.members;
   for (int i = threadIdx.x; i < n; i += TW) {
     const int64_t rr = r - 1 + i / sw, cc = c0 + i % sw;
     if (cc >= f.width) continue;
@@ -421,75 +495,135 @@ __global__ void closed_hist_smem_kernel(FieldView f, Window w, double* pmin, dou
     double lo, hi;
     const bool deg = load_bounds(f, at, lo, hi);
     const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at), lo, hi, h) : 0;
-    for (int b = 0; b < h; ++b) T.wn[b * n + i] = load_weight(f, at, b, deg, dbin);
-    const double total = pairwise_sum([&](int b) { return T.wn[b * n + i]; }, h);
+    for (int b = 0; b < h; ++b) {
+      double wb;
+      if (f.wmode == CPB_WEIGHTS_F64) {
+        wb = __ldg(static_cast<const double*>(f.weights) + (int64_t)b * f.wstride + at);
+      } else if (deg) {
+        wb = b == dbin ? 1.0 : 0.0;
+      } else {
+        const unsigned cnt = f.wmode == CPB_WEIGHTS_U8
+            ? (unsigned)__ldg(static_cast<const uint8_t*>(f.weights) + (int64_t)b * f.wstride + at)
+            : (unsigned)__ldg(static_cast<const uint16_t*>(f.weights) + (int64_t)b * f.wstride + at);
+        wb = (double)cnt * invM;  // count / M to within an ulp (closed-form tolerance)
+      }
+      sm[o_wn + b * n + i] = wb;
+    }
+    const double total = pairwise_sum([&](int b) { return sm[o_wn + b * n + i]; }, h);
     const double it = 1.0 / total;
-    for (int b = 0; b < h; ++b) T.wn[b * n + i] *= it;
-    T.lo[i] = lo;
-    T.hi[i] = hi;
-    T.width[i] = hi - lo;
-    T.binw[i] = (hi - lo) / (double)h;
-    T.ibinw[i] = 1.0 / T.binw[i];
+    for (int b = 0; b < h; ++b) sm[o_wn + b * n + i] *= it;
+    sm[i] = lo;
+    sm[o_hi + i] = hi;
+    sm[o_ib + i] = 1.0 / ((hi - lo) / (double)h);
   }
   __syncthreads();
   const int t = threadIdx.x;
   const int64_t c = c0 + 1 + t;
   if (c >= f.width - 1) return;
   const int64_t idx = r * f.width + c;
-  const int li[5] = {sw + t + 1, sw + t + 2, t + 1, sw + t, 2 * sw + t + 1};  // C E N W S
-  double lo[5], hi[5];
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  const double dh = (double)h;
+  const int ic = sw + t + 1;
+  const double x0 = sm[ic], xend = sm[o_hi + ic];
+  bool fast = true;  // see kFastRatio: all five |x| / bin width within bounds
+  {
+    const int li[5] = {sw + t + 1, sw + t + 2, t + 1, sw + t, 2 * sw + t + 1};
 #pragma unroll
-  for (int p = 0; p < 5; ++p) {
-    lo[p] = T.lo[li[p]];
-    hi[p] = T.hi[li[p]];
+    for (int p = 0; p < 5; ++p)
+      fast &= (fabs(sm[li[p]]) + fabs(sm[o_hi + li[p]])) * sm[o_ib + li[p]] <= kFastRatio;
   }
-  const Ranges rg = make_ranges(lo, hi);
-  const double x0 = lo[C_], xend = hi[C_];
-  NState st[5];
+  Nb nb[5];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
-    st[p].j = -1; st[p].cum = 0.0; st[p].wj = 0.0; st[p].c = 0.0; st[p].s = 0.0; st[p].e = 0.0;
-    st[p].next = lo[p];
-    while (st[p].next <= x0) nb_enter(T, li[p], h, hi[p], st[p]);
+    const int li = p == E_ ? sw + t + 2 : (p == N_ ? t + 1 : (p == W_ ? sw + t : 2 * sw + t + 1));
+    Nb& q = nb[p];
+    q.i = li;
+    q.lo = sm[li];
+    q.width = sm[o_hi + li] - q.lo;
+    q.binw = q.width / dh;
+    q.j = -1; q.c = 0.0; q.s = 0.0; q.e = 0.0;
+    q.next = q.lo;
   }
-  const int ic = li[C_];
+  // one merge step of neighbour q, applied when `adv` (selects, no branches)
+  auto step = [&](Nb& q, bool adv) {
+    const int j1 = q.j + 1;
+    const bool in = j1 < h;
+    const double w1 = sm[o_wn + (in ? j1 : h - 1) * n + q.i];
+    const double w0 = (q.j >= 0 && q.j < h) ? sm[o_wn + q.j * n + q.i] : 0.0;
+    const double kh = sm[o_kh + (j1 + 1 < h ? j1 + 1 : h)];
+    const double nxt = j1 + 1 < h ? fma(q.width, kh, q.lo) : (j1 + 1 == h ? sm[o_hi + q.i] : inf);
+    const double c1 = q.c + w0;                          // np.cumsum order
+    const double e1 = fma(q.binw, (double)j1, q.lo);     // lo + binw * j (distributions.py:97)
+    q.j = adv ? j1 : q.j;
+    q.c = adv ? (in ? c1 : 1.0) : q.c;
+    q.s = adv ? (in ? w1 * sm[o_ib + q.i] : 0.0) : q.s;
+    q.e = adv ? (in ? e1 : 0.0) : q.e;
+    q.next = adv ? (in ? nxt : inf) : q.next;
+  };
+#pragma unroll
+  for (int p = 1; p < 5; ++p)
+    while (nb[p].next <= x0) step(nb[p], true);
+  const double cwidth = xend - x0, cibinw = sm[o_ib + ic];
   int jc = 0;
-  double pdf = T.wn[ic] * T.ibinw[ic];
-  double nextc = h > 1 ? T.lo[ic] + T.width[ic] * T.kh[1] : xend;
+  double pdf = sm[o_wn + ic] * cibinw;
+  double nextc = h > 1 ? fma(cwidth, sm[o_kh + 1], x0) : xend;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   double x = x0;
   while (x < xend) {
-    const double xn = dmin(dmin(nextc, dmin(st[E_].next, st[N_].next)), dmin(st[W_].next, st[S_].next));
-    if (xn > x) {
-      const double half = 0.5 * (xn - x), mid = 0.5 * (xn + x);
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const double xn =
+        dmin(dmin(nextc, dmin(nb[E_].next, nb[N_].next)), dmin(nb[W_].next, nb[S_].next));
+    // the piece [x, xn]; coincident edges give a zero-width piece worth exactly 0
+    const double half = 0.5 * (xn - x), mid = 0.5 * (xn + x);
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (fast) {
+      double Fm[5], F[5], g[4];
+      const double tau = half * GL3::x(2);
+#pragma unroll
+      for (int p = 1; p < 5; ++p) Fm[p] = fma(mid - nb[p].e, nb[p].s, nb[p].c);
+      integrands(Fm, g);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q] = GL3::w(1) * g[q];
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+#pragma unroll
+        for (int p = 1; p < 5; ++p) F[p] = fma(side ? tau : -tau, nb[p].s, Fm[p]);
+        integrands(F, g);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(0), g[q], s[q]);
+      }
+    } else {
 #pragma unroll
       for (int j = 0; j < GL3::n; ++j) {
         const double xx = node_x(mid, half, GL3::x(j));
         double F[5], g[4];
 #pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = fma(xx - st[p].e, st[p].s, st[p].c);
+        for (int p = 1; p < 5; ++p) F[p] = fma(xx - nb[p].e, nb[p].s, nb[p].c);
         integrands(F, g);
 #pragma unroll
         for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(j), g[q], s[q]);
       }
-      const double scale = pdf * half;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (x >= rg.lo[q] && xn <= rg.hi[q]) acc[q] = fma(s[q], scale, acc[q]);
     }
-    if (nextc == xn) {
-      ++jc;
-      if (jc >= h) {
-        nextc = __longlong_as_double(0x7ff0000000000000ll);
-      } else {
-        pdf = T.wn[jc * n + ic] * T.ibinw[ic];
-        nextc = jc + 1 >= h ? xend : T.lo[ic] + T.width[ic] * T.kh[jc + 1];
-      }
+    bool m[4];
+    range_masks(nb[E_].j < 0, nb[N_].j < 0, nb[W_].j < 0, nb[S_].j < 0, nb[E_].j >= h,
+                nb[N_].j >= h, nb[W_].j >= h, nb[S_].j >= h, m);
+    const double scale = pdf * half;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double add = fma(s[q], scale, acc[q]);
+      acc[q] = m[q] ? add : acc[q];
+    }
+    {  // centre list
+      const bool adv = nextc == xn;
+      const int j1 = jc + 1;
+      const double pdf1 = sm[o_wn + (j1 < h ? j1 : h - 1) * n + ic] * cibinw;
+      const double kh = sm[o_kh + (j1 + 1 < h ? j1 + 1 : h)];
+      const double nx1 = j1 + 1 < h ? fma(cwidth, kh, x0) : (j1 + 1 == h ? xend : inf);
+      jc = adv ? j1 : jc;
+      pdf = adv ? pdf1 : pdf;
+      nextc = adv ? nx1 : nextc;
     }
 #pragma unroll
-    for (int p = 1; p < 5; ++p)
-      if (st[p].next == xn) nb_enter(T, li[p], h, hi[p], st[p]);
+    for (int p = 1; p < 5; ++p) step(nb[p], nb[p].next == xn);
     x = dmax(x, xn);
   }
   store(pmin, pmax, psad, idx, acc);
@@ -523,15 +657,18 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
         break;
       }
       // tile width so the staged float64 weights fit comfortably in shared memory
-      int tw = 128;
-      while (tw > 32 && (size_t)(5 + f.bins) * 3 * (tw + 2) * 8 > 64 * 1024) tw >>= 1;
+      int tw = kHistThreads;
+      while (tw > 32 && (size_t)(3 + f.bins) * 3 * (tw + 2) * 8 > 64 * 1024) tw >>= 1;
       Window wh = w;
       wh.ntiles = (int)((f.width - 2 + tw - 1) / tw);
       const int64_t hb = rows * wh.ntiles;
-      const size_t smem = ((size_t)(5 + f.bins) * 3 * (tw + 2) + f.bins + 1) * 8;
+      const size_t smem = ((size_t)(3 + f.bins) * 3 * (tw + 2) + f.bins + 1) * 8;
+      // CPB_HIST_MINB picks the register budget variant (experiments; default 3 blocks/SM)
+      static const int minb = [] { const char* e = getenv("CPB_HIST_MINB"); return e ? atoi(e) : 4; }();
+      auto kern = minb >= 6 ? closed_hist_smem_kernel<6> : (minb == 5 ? closed_hist_smem_kernel<5> : (minb == 4 ? closed_hist_smem_kernel<4> : closed_hist_smem_kernel<3>));
       if (smem > 48 * 1024)
-        cudaFuncSetAttribute(closed_hist_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      closed_hist_smem_kernel<<<(unsigned)hb, tw, smem, st>>>(f, wh, pmin, pmax, psad);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      kern<<<(unsigned)hb, tw, smem, st>>>(f, wh, pmin, pmax, psad);
       break;
     }
     default:
