@@ -9,6 +9,8 @@
 // (__dadd_rn, __dmul_rn, ...) so no FMA contraction changes a result, and
 // the member reductions run in member order exactly like numpy's axis-0
 // reductions (sequential).  min/max and bin counts are exact.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "cpb_common.cuh"
@@ -232,7 +234,9 @@ CPB_D float bin_threshold(int k, double lo, double scale) {
   return c;
 }
 
-template <int KIND>
+// NT: histogram bin count handled with NT-1 register thresholds (1..kThreshBins),
+// or 0 for the shared-memory counters (more bins).
+template <int KIND, int NT>
 __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                            FitArgs a, int stages, int mbox,
                                                            int nbox, int64_t ntiles) {
@@ -292,20 +296,20 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
         const int h = a.bins;
         const double dlo = (double)lo;
         const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
-        uint32_t c[kThreshBins + 1];
-        if (h <= kThreshBins) {
+        constexpr int NB = NT > 0 ? NT : 1;
+        uint32_t c[NB + 1];
+        if (NT > 0) {
           // cumulative counts C_k = #{v >= thr_k}; bin b holds C_b - C_{b+1}
-          float thr[kThreshBins];
+          float thr[NB];
 #pragma unroll
-          for (int q = 1; q < kThreshBins; ++q)
-            thr[q] = (q < h && hi > lo) ? bin_threshold(q, dlo, scale) : __int_as_float(0x7f800000);
+          for (int q = 1; q < NB; ++q) thr[q] = hi > lo ? bin_threshold(q, dlo, scale) : 0.0f;
 #pragma unroll
-          for (int q = 0; q <= kThreshBins; ++q) c[q] = 0u;
+          for (int q = 0; q <= NB; ++q) c[q] = 0u;
 #pragma unroll 4
           for (int m = 0; m < M; ++m) {
             const float x = col[m * kTmaTile];
 #pragma unroll
-            for (int q = 1; q < kThreshBins; ++q) c[q] += (x >= thr[q]) ? 1u : 0u;
+            for (int q = 1; q < NB; ++q) c[q] += (x >= thr[q]) ? 1u : 0u;
           }
           c[0] = (uint32_t)M;
         } else {
@@ -314,25 +318,23 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
             for (int m = 0; m < M; ++m) cnt[bin_of(col[m * kTmaTile], dlo, scale, h) * kTmaTile + tid] += 1u;
         }
         const bool flat = !(hi > lo);  // degenerate: counts resolved at use, once eps is known
-        auto count = [&](int b) -> uint32_t {
-          if (flat) return 0u;
-          if (h <= kThreshBins) {
-            uint32_t cb = 0u, cn = 0u;
+        if (NT > 0) {
 #pragma unroll
-            for (int q = 0; q <= kThreshBins; ++q) {
-              if (q == b) cb = c[q];
-              if (q == b + 1) cn = c[q];
-            }
-            return b + 1 >= h ? cb : cb - cn;
+          for (int b = 0; b < NB; ++b) {
+            const uint32_t v = flat ? 0u : (b + 1 < NB ? c[b] - c[b + 1] : c[b]);
+            if (a.wmode == CPB_WEIGHTS_U8)
+              static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
+            else
+              static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
           }
-          return cnt[b * kTmaTile + tid];
-        };
-        if (a.wmode == CPB_WEIGHTS_U8) {
-          uint8_t* dst = static_cast<uint8_t*>(a.counts);
-          for (int b = 0; b < h; ++b) dst[(int64_t)b * a.wstride + p] = (uint8_t)count(b);
         } else {
-          uint16_t* dst = static_cast<uint16_t*>(a.counts);
-          for (int b = 0; b < h; ++b) dst[(int64_t)b * a.wstride + p] = (uint16_t)count(b);
+          for (int b = 0; b < h; ++b) {
+            const uint32_t v = flat ? 0u : cnt[b * kTmaTile + tid];
+            if (a.wmode == CPB_WEIGHTS_U8)
+              static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
+            else
+              static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
+          }
         }
       }
       if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) {
@@ -492,7 +494,8 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
   const bool tma_ok = (mstride % 4 == 0) && ((reinterpret_cast<uintptr_t>(ens) & 15) == 0) &&
                       tile_bytes * 2 + cnt_bytes + 64 <= 200 * 1024;
   if (tma_ok) {
-    const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, (96 * 1024) / tile_bytes));
+    static const int stage_kb = [] { const char* e = getenv("CPB_FIT_STAGE_KB"); return e ? atoi(e) : 64; }();
+    const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, ((size_t)stage_kb * 1024) / tile_bytes));
     const size_t smem = stages * tile_bytes + stages * 8 + cnt_bytes;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -516,25 +519,41 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
         return CPB_ECUDA;
       }
       const int64_t ntiles = (n + kTmaTile - 1) / kTmaTile;
-#define CPB_FIT_TMA(K)                                                                           \
-  case K: {                                                                                      \
-    auto kern = fit_tma_kernel<K>;                                                               \
+#define CPB_FIT_TMA_LAUNCH(KERN)                                                                 \
+  do {                                                                                           \
+    auto kern = KERN;                                                                            \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
     int per_sm = 1;                                                                              \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaTile, smem);                \
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
     kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);            \
-    break;                                                                                       \
-  }
+  } while (0)
+#define CPB_FIT_TMA(K) \
+  case K:              \
+    CPB_FIT_TMA_LAUNCH((fit_tma_kernel<K, 0>)); \
+    break;
       switch (f->kind) {
         CPB_FIT_TMA(CPB_UNIFORM)
         CPB_FIT_TMA(CPB_EPANECHNIKOV)
-        CPB_FIT_TMA(CPB_HISTOGRAM)
         CPB_FIT_TMA(CPB_GAUSSIAN)
+        case CPB_HISTOGRAM:
+          switch (f->bins <= kThreshBins ? f->bins : 0) {
+            case 1: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 1>)); break;
+            case 2: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 2>)); break;
+            case 3: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 3>)); break;
+            case 4: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 4>)); break;
+            case 5: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 5>)); break;
+            case 6: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 6>)); break;
+            case 7: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 7>)); break;
+            case 8: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 8>)); break;
+            default: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 0>)); break;
+          }
+          break;
         default:
           set_error("unknown model kind %d", f->kind);
           return CPB_EINVAL;
       }
+#undef CPB_FIT_TMA_LAUNCH
 #undef CPB_FIT_TMA
       CPB_CHECK_LAUNCH("fit kernel (TMA)");
     }
