@@ -100,6 +100,9 @@ typedef struct cpb_field {
   int64_t plane_stride;  /* elements between histogram bin planes; 0 = height * width.  Lets a
                             slab view (offset base pointers, fewer rows) address the bin planes
                             of a taller allocation, e.g. a row slab with halo rows */
+  const double* eps_device; /* optional device pointer: when set, kernels read eps from it
+                            instead of `eps` (no host round trip between fit and classify;
+                            filled by cpb_pair_to_eps) */
   double eps;            /* from the GLOBAL ensemble range (distributions.py:30-36) */
   double k;              /* epanechnikov k (fields.py:31) */
   void* lo;
@@ -137,6 +140,14 @@ double cpb_epsilon(double gmin, double gmax);
  */
 int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
             int32_t accumulate, void* stream);
+
+/* Device-side eps, no host synchronisation: cpb_range_to_pair turns the
+ * d_range words of cpb_fit into d_pair = {-min, max} (float64; NaN when a
+ * value was non-finite), ready for a MAX all-reduce across row slabs;
+ * cpb_pair_to_eps writes eps = max(1e-12, 1e-9 * (max - min)) to d_eps
+ * (distributions.py:30-36), for cpb_field.eps_device. */
+int cpb_range_to_pair(const uint32_t* d_range, double* d_pair, void* stream);
+int cpb_pair_to_eps(const double* d_pair, double* d_eps, void* stream);
 
 /* Synchronously read back a d_range written by cpb_fit; returns
  * CPB_ENONFINITE if any value was NaN/Inf. */

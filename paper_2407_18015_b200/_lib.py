@@ -31,7 +31,7 @@ class CpbField(ctypes.Structure):
         ("kind", c_i32), ("bins", c_i32), ("members", c_i32), ("bounds", c_i32),
         ("weights_mode", c_i32), ("reserved", c_i32),
         ("height", c_i64), ("width", c_i64), ("row0", c_i64), ("global_width", c_i64),
-        ("plane_stride", c_i64),
+        ("plane_stride", c_i64), ("eps_device", c_vp),
         ("eps", c_dbl), ("k", c_dbl),
         ("lo", c_vp), ("hi", c_vp), ("mean", c_vp), ("spread", c_vp),
         ("weights", c_vp), ("weight_table", c_vp),
@@ -45,6 +45,8 @@ _SIGNATURES = {
     "cpb_field_plane_bytes": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
     "cpb_fit": (c_i32, [c_vp, c_i64, ctypes.POINTER(CpbField), c_vp, c_i32, c_vp]),
     "cpb_read_range": (c_i32, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), c_vp]),
+    "cpb_range_to_pair": (c_i32, [c_vp, c_vp, c_vp]),
+    "cpb_pair_to_eps": (c_i32, [c_vp, c_vp, c_vp]),
     "cpb_from_scalar": (c_i32, [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
     "cpb_classify_closed": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "cpb_classify_mc": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_u64, c_i64, c_i32,

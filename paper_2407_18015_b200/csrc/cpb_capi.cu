@@ -16,6 +16,8 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
                cudaStream_t st);
 int launch_from_scalar(const double* v, int64_t n, double half, double* lo, double* hi,
                        cudaStream_t st);
+int launch_range_to_pair(const uint32_t* range, double* pair, cudaStream_t st);
+int launch_pair_to_eps(const double* pair, double* eps, cudaStream_t st);
 int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cudaStream_t st);
 int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
                  int64_t height, double amp, uint64_t seed, cudaStream_t st);
@@ -123,6 +125,16 @@ int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* st
   if (gmin) *gmin = (double)ordered_to_float(h[0]);
   if (gmax) *gmax = (double)ordered_to_float(h[1]);
   return CPB_OK;
+}
+
+int cpb_range_to_pair(const uint32_t* d_range, double* d_pair, void* stream) {
+  if (!d_range || !d_pair) { set_error("NULL range or pair pointer"); return CPB_EINVAL; }
+  return launch_range_to_pair(d_range, d_pair, (cudaStream_t)stream);
+}
+
+int cpb_pair_to_eps(const double* d_pair, double* d_eps, void* stream) {
+  if (!d_pair || !d_eps) { set_error("NULL pair or eps pointer"); return CPB_EINVAL; }
+  return launch_pair_to_eps(d_pair, d_eps, (cudaStream_t)stream);
 }
 
 int cpb_from_scalar(const double* d_values, int64_t height, int64_t width, double error_bound,

@@ -629,31 +629,54 @@ __global__ void __launch_bounds__(kHistThreads, MINB) closed_hist_smem_kernel(
   store(pmin, pmax, psad, idx, acc);
 }
 
-// Table-driven histogram stencil (the production path while its tables fit in
-// shared memory).  A block computes a TH x TW tile of vertices.  It stages the
-// (TH + 2) x (TW + 2) pixels around the tile as per-pixel STATE TABLES: for
-// every position k in the merged sweep (k = 0 below the support, k = b + 1
-// inside bin b, k = h + 1 above) the CDF on that stretch is
+// Table-driven histogram stencil (the production path for bins <= kTabMaxBins).
+// A block computes a TH x TW tile of vertices.  It stages the (TH + 2) x
+// (TW + 2) pixels around the tile as per-pixel STATE TABLES: for every
+// position k in the merged sweep (k = 0 below the support, k = b + 1 inside
+// bin b, k = h + 1 above) the CDF on that stretch is
 // F(x) = CUM[k] + SL[k] (x - EV[k]) and the next edge ahead is NX[k].  CUM is
 // the sequential prefix sum of wn = w / sum(w) (np.cumsum and numpy pairwise
 // sum orders, engine.py:538-540), SL = wn / binw, EV = lo + binw b
 // (distributions.py:97) and NX the kinks of engine.py:570-571 (the last one is
 // the support end itself).  The sweep over the five sorted edge lists then
-// only increments integer positions and re-reads four table entries, with no
-// floating-point bookkeeping and no divergent branches.
-constexpr int kTabTW = 32, kTabTH = 8;
+// only increments integer positions and re-reads four table entries (one
+// address, constant offsets), with no floating-point bookkeeping and no
+// divergent branches.
+constexpr int kTabTW = 32, kTabTH = 8, kTabMaxBins = 16;
+constexpr int kTabSW = kTabTW + 2, kTabP = kTabSW * (kTabTH + 2);
+
+// numpy pairwise summation of w[0..n) for n <= 16 (register array, unrolled)
+CPB_D double pairwise16(const double* w, int n) {
+  if (n < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < n) r = __dadd_rn(r, w[i]);
+    return r;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = w[j];
+  if (n == 16) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], w[8 + j]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+  for (int i = 8; i < 16; ++i)
+    if (n < 16 && i < n) res = __dadd_rn(res, w[i]);
+  return res;
+}
 
 __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     FieldView f, int64_t row_begin, int64_t row_end, int ctiles, double* pmin, double* pmax,
     double* psad) {
   extern __shared__ double sm[];
-  constexpr int SW = kTabTW + 2, SH = kTabTH + 2, P = SW * SH;
-  const int h = f.bins, K = h + 2;
-  double* CUM = sm;
-  double* SL = CUM + K * P;
-  double* EV = SL + K * P;
-  double* NX = EV + K * P;
-  double* RATIO = NX + K * P;  // (|lo| + |hi|) / binw, for the fast-mode test
+  constexpr int P = kTabP, SW = kTabSW;
+  const int h = f.bins;
+  double* T = sm;                          // [(h + 2) states][4 fields][P pixels]
+  double* RATIO = sm + (size_t)(h + 2) * 4 * P;  // (|lo| + |hi|) / binw, fast-mode test
   const int64_t r0 = row_begin + (int64_t)(blockIdx.x / ctiles) * kTabTH;
   const int64_t c0 = (int64_t)(blockIdx.x % ctiles) * kTabTW;  // staged cols [c0, c0 + SW)
   const int tid = threadIdx.y * kTabTW + threadIdx.x;
@@ -666,37 +689,42 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     double lo, hi;
     const bool deg = load_bounds(f, at, lo, hi);
     const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at), lo, hi, h) : 0;
-    // raw weights into SL[1..h] as scratch, then the tables
-    for (int b = 0; b < h; ++b) {
-      double wb;
-      if (f.wmode == CPB_WEIGHTS_F64) {
-        wb = __ldg(static_cast<const double*>(f.weights) + (int64_t)b * f.wstride + at);
-      } else if (deg) {
-        wb = b == dbin ? 1.0 : 0.0;
-      } else {
-        const unsigned cnt = f.wmode == CPB_WEIGHTS_U8
-            ? (unsigned)__ldg(static_cast<const uint8_t*>(f.weights) + (int64_t)b * f.wstride + at)
-            : (unsigned)__ldg(static_cast<const uint16_t*>(f.weights) + (int64_t)b * f.wstride + at);
-        wb = (double)cnt * invM;  // count / M to within an ulp (closed-form tolerance)
+    double wv[kTabMaxBins];
+#pragma unroll
+    for (int b = 0; b < kTabMaxBins; ++b) {
+      double wb = 0.0;
+      if (b < h) {
+        if (f.wmode == CPB_WEIGHTS_F64) {
+          wb = __ldg(static_cast<const double*>(f.weights) + (int64_t)b * f.wstride + at);
+        } else if (deg) {
+          wb = b == dbin ? 1.0 : 0.0;
+        } else {
+          const unsigned cnt = f.wmode == CPB_WEIGHTS_U8
+              ? (unsigned)__ldg(static_cast<const uint8_t*>(f.weights) + (int64_t)b * f.wstride + at)
+              : (unsigned)__ldg(static_cast<const uint16_t*>(f.weights) + (int64_t)b * f.wstride + at);
+          wb = (double)cnt * invM;  // count / M to within an ulp (closed-form tolerance)
+        }
       }
-      SL[(b + 1) * P + i] = wb;
+      wv[b] = wb;
     }
-    const double total = pairwise_sum([&](int b) { return SL[(b + 1) * P + i]; }, h);
-    const double it = 1.0 / total;
+    const double it = 1.0 / pairwise16(wv, h);
     const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
+    T[0 * P + i] = 0.0; T[1 * P + i] = 0.0; T[2 * P + i] = 0.0; T[3 * P + i] = lo;
     double cum = 0.0;
-    CUM[i] = 0.0; SL[i] = 0.0; EV[i] = 0.0; NX[i] = lo;
-    for (int b = 0; b < h; ++b) {
-      const double wn = SL[(b + 1) * P + i] * it;
-      const int k = b + 1;
-      CUM[k * P + i] = cum;
-      SL[k * P + i] = wn * ibinw;
-      EV[k * P + i] = fma(binw, (double)b, lo);
-      NX[k * P + i] = b + 1 < h ? fma(width, (double)(b + 1) / dh, lo) : hi;
-      cum += wn;
+#pragma unroll
+    for (int b = 0; b < kTabMaxBins; ++b) {
+      if (b < h) {
+        const double wn = wv[b] * it;
+        double* t = T + (size_t)(b + 1) * 4 * P + i;
+        t[0] = cum;
+        t[P] = wn * ibinw;
+        t[2 * P] = fma(binw, (double)b, lo);
+        t[3 * P] = b + 1 < h ? fma(width, (double)(b + 1) / dh, lo) : hi;
+        cum += wn;
+      }
     }
-    CUM[(h + 1) * P + i] = 1.0; SL[(h + 1) * P + i] = 0.0; EV[(h + 1) * P + i] = 0.0;
-    NX[(h + 1) * P + i] = inf;
+    double* t = T + (size_t)(h + 1) * 4 * P + i;
+    t[0] = 1.0; t[P] = 0.0; t[2 * P] = 0.0; t[3 * P] = inf;
     RATIO[i] = (fabs(lo) + fabs(hi)) * ibinw;
   }
   __syncthreads();
@@ -707,29 +735,31 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   const bool fast = RATIO[ip[0]] <= kFastRatio && RATIO[ip[1]] <= kFastRatio &&
                     RATIO[ip[2]] <= kFastRatio && RATIO[ip[3]] <= kFastRatio &&
                     RATIO[ip[4]] <= kFastRatio;
-  const double x0 = NX[ip[0]];               // lo_C
-  const double xend = NX[h * P + ip[0]];     // hi_C (last edge)
+  constexpr int K4 = 4 * P;
+  const double x0 = T[3 * P + ip[0]];                  // lo_C (NX of state 0)
+  const double xend = T[(size_t)h * K4 + 3 * P + ip[0]];  // hi_C (NX of state h)
   int kp[5];
   double cc_[5], ss[5], ee[5], nx[5];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
     int k = 0;
-    while (NX[k * P + ip[p]] <= x0) ++k;
+    while (T[k * K4 + 3 * P + ip[p]] <= x0) ++k;
     kp[p] = k;
-    cc_[p] = CUM[k * P + ip[p]];
-    ss[p] = SL[k * P + ip[p]];
-    ee[p] = EV[k * P + ip[p]];
-    nx[p] = NX[k * P + ip[p]];
+    const double* t = T + k * K4 + ip[p];
+    cc_[p] = t[0];
+    ss[p] = t[P];
+    ee[p] = t[2 * P];
+    nx[p] = t[3 * P];
   }
   int kc = 1;
-  double pdf = SL[P + ip[0]], nextc = NX[P + ip[0]];
+  double pdf = T[K4 + P + ip[0]], nextc = T[K4 + 3 * P + ip[0]];
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   double x = x0;
   while (x < xend) {
     const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
     // the piece [x, xn]; coincident edges give a zero-width piece worth exactly 0
     const double half = 0.5 * (xn - x), mid = 0.5 * (xn + x);
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    double s[4];
     if (fast) {
       double Fm[5], F[5], g[4];
       const double tau = half * GL3::x(2);
@@ -747,6 +777,8 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
         for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(0), g[q], s[q]);
       }
     } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q] = 0.0;
 #pragma unroll
       for (int j = 0; j < GL3::n; ++j) {
         const double xx = node_x(mid, half, GL3::x(j));
@@ -766,16 +798,19 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     for (int q = 0; q < 4; ++q) acc[q] = m[q] ? fma(s[q], scale, acc[q]) : acc[q];
     // advance every list whose next edge is xn
     kc += nextc == xn ? 1 : 0;
-    pdf = SL[kc * P + ip[0]];
-    nextc = NX[kc * P + ip[0]];
+    {
+      const double* t = T + kc * K4 + ip[0];
+      pdf = t[P];
+      nextc = t[3 * P];
+    }
 #pragma unroll
     for (int p = 1; p < 5; ++p) {
       kp[p] += nx[p] == xn ? 1 : 0;
-      const int o = kp[p] * P + ip[p];
-      cc_[p] = CUM[o];
-      ss[p] = SL[o];
-      ee[p] = EV[o];
-      nx[p] = NX[o];
+      const double* t = T + kp[p] * K4 + ip[p];
+      cc_[p] = t[0];
+      ss[p] = t[P];
+      ee[p] = t[2 * P];
+      nx[p] = t[3 * P];
     }
     x = dmax(x, xn);
   }
@@ -806,9 +841,9 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
       break;
     case CPB_HISTOGRAM: {
-      const size_t tab_smem = ((size_t)4 * (f.bins + 2) + 1) * (kTabTW + 2) * (kTabTH + 2) * 8;
+      const size_t tab_smem = ((size_t)4 * (f.bins + 2) + 1) * kTabP * 8;
       static const int variant = [] { const char* e = getenv("CPB_HIST_VARIANT"); return e ? atoi(e) : 0; }();
-      if (variant == 0 && tab_smem <= 110 * 1024) {
+      if (variant == 0 && f.bins <= kTabMaxBins && tab_smem <= 200 * 1024) {
         const int ctiles = (int)((f.width - 2 + kTabTW - 1) / kTabTW);
         const int64_t rtiles = (rows + kTabTH - 1) / kTabTH;
         cudaFuncSetAttribute(closed_hist_tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem);

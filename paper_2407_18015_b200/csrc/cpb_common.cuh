@@ -185,6 +185,7 @@ struct FieldView {
   int64_t npix;     // height * width
   int64_t wstride;  // elements between histogram bin planes
   double eps, k;
+  const double* eps_dev;
   const void* lo;
   const void* hi;
   const double* mean;
@@ -200,10 +201,13 @@ inline FieldView make_view(const cpb_field& f) {
   v.gwidth = f.global_width; v.npix = f.height * f.width;
   v.wstride = f.plane_stride > 0 ? f.plane_stride : v.npix;
   v.eps = f.eps; v.k = f.k;
+  v.eps_dev = f.eps_device;
   v.lo = f.lo; v.hi = f.hi; v.mean = f.mean; v.spread = f.spread; v.weights = f.weights;
   v.wtab = f.weight_table;
   return v;
 }
+
+CPB_D double field_eps(const FieldView& v) { return v.eps_dev ? __ldg(v.eps_dev) : v.eps; }
 
 // Support bounds of a uniform/histogram pixel, widened like fields.py:140-143
 // when the stored (fitted, f32) range is degenerate.  Returns true if widened.
@@ -216,7 +220,7 @@ CPB_D bool load_bounds(const FieldView& v, int64_t idx, double& lo, double& hi) 
   lo = (double)__ldg(static_cast<const float*>(v.lo) + idx);
   hi = (double)__ldg(static_cast<const float*>(v.hi) + idx);
   if (hi <= lo) {
-    const double c = lo, h = __dmul_rn(0.5, v.eps);
+    const double c = lo, h = __dmul_rn(0.5, field_eps(v));
     lo = __dsub_rn(c, h);
     hi = __dadd_rn(c, h);
     return true;
@@ -228,7 +232,7 @@ CPB_D bool load_bounds(const FieldView& v, int64_t idx, double& lo, double& hi) 
 CPB_D void load_epan(const FieldView& v, int64_t idx, double& m, double& hw) {
   m = __ldg(v.mean + idx);
   const double s = __ldg(v.spread + idx);
-  const double a = __dmul_rn(v.k, s), b = __dmul_rn(0.5, v.eps);
+  const double a = __dmul_rn(v.k, s), b = __dmul_rn(0.5, field_eps(v));
   hw = a > b ? a : (b > a ? b : a);  // np.maximum (no NaN inputs here)
 }
 

@@ -358,6 +358,20 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
   merge_range(vmin, vmax, bad, a.range);
 }
 
+// d_range words -> {-min, max} as float64 (NaN if a value was non-finite)
+__global__ void range_pair_kernel(const uint32_t* range, double* pair) {
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  pair[0] = range[2] ? nan : -(double)ordered_to_float(range[0]);
+  pair[1] = range[2] ? nan : (double)ordered_to_float(range[1]);
+}
+
+// eps = max(1e-12, 1e-9 * (max - min))  (distributions.py:30-36)
+__global__ void pair_eps_kernel(const double* pair, double* eps) {
+  const double spread = pair[1] + pair[0];  // max - min, pair[0] = -min
+  const double e = 1e-9 * spread;
+  *eps = e != e ? e : (e > 1e-12 ? e : 1e-12);
+}
+
 __global__ void range_init_kernel(uint32_t* range) {
   range[0] = 0xffffffffu;
   range[1] = 0u;
@@ -591,6 +605,18 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
   }
 #undef CPB_FIT_CASE
   CPB_CHECK_LAUNCH("fit kernel");
+  return CPB_OK;
+}
+
+int launch_range_to_pair(const uint32_t* range, double* pair, cudaStream_t st) {
+  range_pair_kernel<<<1, 1, 0, st>>>(range, pair);
+  CPB_CHECK_LAUNCH("range pair kernel");
+  return CPB_OK;
+}
+
+int launch_pair_to_eps(const double* pair, double* eps, cudaStream_t st) {
+  pair_eps_kernel<<<1, 1, 0, st>>>(pair, eps);
+  CPB_CHECK_LAUNCH("pair eps kernel");
   return CPB_OK;
 }
 

@@ -156,50 +156,88 @@ def _plane_views(dev):
     return out
 
 
+class SlabField:
+    """Halo-padded fitted planes of one rank's slab, reusable across refits.
+
+    ``dev`` is the DeviceField over all local rows (halo rows included);
+    ``view`` a cpb_field over the owned rows only (offset base pointers and
+    the full-height bin-plane stride), which is what cpb_fit writes through.
+    With ``device_eps`` the global eps never visits the host: the fit's range
+    words become a {-min, max} pair on the device, the pair is MAX-all-reduced
+    across ranks (NCCL), and cpb_pair_to_eps writes eps where the stencil
+    kernels read it (cpb_field.eps_device).
+    """
+
+    def __init__(self, model, slab: Slab, width: int, members: int, device, device_eps: bool = True):
+        import torch
+
+        from . import _lib
+        from .fields import DeviceField
+
+        self.model, self.slab, self.width, self.members = model, slab, width, members
+        dev = DeviceField(model.kind, model.bins, members, slab.local_height, width,
+                          row0=slab.local_row0, global_width=width, k=model.k, device=device)
+        dev.allocate_fitted()
+        view = _lib.CpbField.from_buffer_copy(dev.struct)
+        off = slab.halo_top * width
+        for name, esz in (("lo", 4), ("hi", 4), ("mean", 8), ("spread", 8)):
+            base = getattr(dev.struct, name)
+            if base:
+                setattr(view, name, base + off * esz)
+        if dev.struct.weights:
+            view.weights = dev.struct.weights + off * (1 if members <= 255 else 2)
+            view.plane_stride = slab.local_height * width
+        view.height = slab.owned
+        self.dev, self.view = dev, view
+        self.device_eps = device_eps
+        self.pair = torch.zeros(2, dtype=torch.float64, device=device)
+        self.eps_t = torch.zeros(1, dtype=torch.float64, device=device)
+        if device_eps:
+            dev.struct.eps_device = self.eps_t.data_ptr()
+
+    def fit(self, ens_slab, group=None, timer=None):
+        """Fit the owned rows, make the global eps, exchange the halo rows."""
+        import ctypes
+
+        from . import _lib
+
+        lib = _lib.load()
+        s = _lib.stream_ptr()
+        rng = self.dev.tensors["range"].data_ptr()
+        if timer:
+            timer("fit", True)
+        _lib.check(lib.cpb_fit(ens_slab.data_ptr(), self.slab.owned * self.width,
+                               ctypes.byref(self.view), rng, 0, s))
+        if timer:
+            timer("fit", False)
+        st = self.dev.struct
+        st.bounds, st.weights_mode, st.plane_stride = self.view.bounds, self.view.weights_mode, 0
+        if self.device_eps:
+            _lib.check(lib.cpb_range_to_pair(rng, self.pair.data_ptr(), s))
+            _, world = _group_world(group)
+            if world > 1:
+                import torch.distributed as dist
+
+                dist.all_reduce(self.pair, op=dist.ReduceOp.MAX, group=group)
+            _lib.check(lib.cpb_pair_to_eps(self.pair.data_ptr(), self.eps_t.data_ptr(), s))
+        else:
+            gmin, gmax = ctypes.c_double(), ctypes.c_double()
+            _lib.check(lib.cpb_read_range(rng, ctypes.byref(gmin), ctypes.byref(gmax), s))
+            gmin, gmax = allreduce_range(gmin.value, gmax.value, ens_slab.device, group)
+            self.dev.eps = lib.cpb_epsilon(gmin, gmax)
+        exchange_halo_rows(_plane_views(self.dev), self.slab, group)
+        return self.dev
+
+
 def fit_slab(ens_slab, model, slab: Slab, width: int, group=None, timer=None):
     """Fit a rank's owned rows into halo-padded planes; global eps; halo exchange.
 
     ``ens_slab``: (M, owned, W) float32 CUDA tensor of rows [row_begin, row_end).
     Returns the DeviceField (local_height rows; local row 0 is global row
-    ``slab.local_row0``).
+    ``slab.local_row0``); its eps is a host value (synchronous path).
     """
-    import ctypes
-
-    from . import _lib
-    from .fields import DeviceField
-
-    lib = _lib.load()
-    M = int(ens_slab.shape[0])
-    dev = DeviceField(model.kind, model.bins, M, slab.local_height, width, row0=slab.local_row0,
-                      global_width=width, k=model.k, device=ens_slab.device)
-    dev.allocate_fitted()
-    # a view of the owned rows inside the padded planes
-    view = _lib.CpbField.from_buffer_copy(dev.struct)
-    off = slab.halo_top * width
-    for name, esz in (("lo", 4), ("hi", 4), ("mean", 8), ("spread", 8)):
-        base = getattr(dev.struct, name)
-        if base:
-            setattr(view, name, base + off * esz)
-    if dev.struct.weights:
-        view.weights = dev.struct.weights + off * (1 if M <= 255 else 2)
-        view.plane_stride = slab.local_height * width
-    view.height = slab.owned
-    s = _lib.stream_ptr()
-    rng = dev.tensors["range"].data_ptr()
-    if timer:
-        timer("fit", True)
-    _lib.check(lib.cpb_fit(ens_slab.data_ptr(), slab.owned * width, ctypes.byref(view), rng, 0, s))
-    if timer:
-        timer("fit", False)
-    dev.struct.bounds = view.bounds
-    dev.struct.weights_mode = view.weights_mode
-    dev.struct.plane_stride = 0
-    gmin, gmax = ctypes.c_double(), ctypes.c_double()
-    _lib.check(lib.cpb_read_range(rng, ctypes.byref(gmin), ctypes.byref(gmax), s))
-    gmin, gmax = allreduce_range(gmin.value, gmax.value, ens_slab.device, group)
-    dev.eps = lib.cpb_epsilon(gmin, gmax)
-    exchange_halo_rows(_plane_views(dev), slab, group)
-    return dev
+    sf = SlabField(model, slab, width, int(ens_slab.shape[0]), ens_slab.device, device_eps=False)
+    return sf.fit(ens_slab, group, timer)
 
 
 def classify_slab(dev, slab: Slab, estimator, channels=("min", "max", "saddle"), out=None,
