@@ -250,10 +250,11 @@ def run_ours(args):
         t = statistics.mean(times)
         if what == "fit":
             nbytes = owned_px * (4 * M + param_bytes(kind, bins))
-            name = f"fit_reg_kernel<{kind}>"
+            name = f"fit_tma_kernel<{kind}>"
         else:
             nbytes = st_verts * (param_bytes(kind, bins) + 24)
-            name = f"closed_{'uniform' if kind == 'uniform' else ('epan' if kind == 'epanechnikov' else 'hist')}_kernel"
+            name = {"uniform": "closed_uniform_kernel", "epanechnikov": "closed_epan_kernel",
+                    "histogram": "closed_hist_tab_kernel"}[kind]
         kern[(kind, what)] = {"kernel": name, "ms": t, "bytes": nbytes, "gbs": nbytes / (t / 1e3) / 1e9}
     dom = max(kern.values(), key=lambda r: r["ms"])
     traffic = None

@@ -182,6 +182,17 @@ int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint
                     double* d_psaddle, int64_t* d_counts, void* stream);
 
 /*
+ * Semianalytical estimator, histogram fields only (engine.py:416-459, grid
+ * chunk engine.py:669-683): c centre draws from the keyed stream (plane 0,
+ * the same draws as the reference), exact neighbour CDFs at each draw, the
+ * conditional pattern probabilities averaged.  Per-draw arithmetic repeats
+ * numpy's; the mean re-associates numpy's pairwise sum (~1e-16 relative).
+ */
+int cpb_classify_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,
+                      int64_t c, double* d_pmin, double* d_pmax, double* d_psaddle,
+                      void* stream);
+
+/*
  * Reference-layout float64 parameters (fields.py:86-103, what from_ensemble
  * returns): uniform/histogram -> d_a = lo, d_b = hi (widened),
  * d_weights = (H, W, bins) weights; epanechnikov -> d_a = mean,

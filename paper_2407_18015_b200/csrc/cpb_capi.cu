@@ -27,6 +27,8 @@ int launch_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t s
               int rng, double* pmin, double* pmax, double* psad, int64_t* counts, cudaStream_t st);
 int launch_unit_block(uint64_t seed, const uint64_t* px, int64_t npix, int planes, int64_t start,
                       int64_t n, double* out, cudaStream_t st);
+int launch_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t c,
+                double* pmin, double* pmax, double* psad, cudaStream_t st);
 
 static thread_local char g_err[512] = "";
 
@@ -178,6 +180,22 @@ int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint
   }
   return launch_mc(f, row_begin, row_end, seed, n_samples, rng, d_pmin, d_pmax, d_psaddle,
                    d_counts, (cudaStream_t)stream);
+}
+
+int cpb_classify_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,
+                      int64_t c, double* d_pmin, double* d_pmax, double* d_psaddle,
+                      void* stream) {
+  int s = check_field(f, true);
+  if (s) return s;
+  if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
+    if (row_end > row_begin) {
+      set_error("rows [%lld, %lld) need a one-row halo inside the field",
+                (long long)row_begin, (long long)row_end);
+      return CPB_EINVAL;
+    }
+  }
+  return launch_semi(f, row_begin, row_end, seed, c, d_pmin, d_pmax, d_psaddle,
+                     (cudaStream_t)stream);
 }
 
 int cpb_materialize(const cpb_field* f, double* d_a, double* d_b, double* d_weights,

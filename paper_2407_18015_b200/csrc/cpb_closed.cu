@@ -329,6 +329,185 @@ __global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
   store(pmin, pmax, psad, idx, acc);
 }
 
+// One Epanechnikov piece [a, b]: s[r] = GL8 sum of integrand r (before the
+// factor half), with the piece's range-membership mask.
+template <bool FAST>
+CPB_D void epan_piece(double a, double b, const double* m, const double* ih, const double* lo,
+                      const double* hi, double s[4], bool mk[4]) {
+  const double pdf0 = 0.75 * ih[C_];
+  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+  bool bl[5], ab[5];
+  double al[5], be[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
+    const bool in = !(bl[p] | ab[p]);
+    be[p] = in ? ih[p] : 0.0;
+    al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (ab[p] ? 1.0 : -1.0);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) s[r] = 0.0;
+  if (FAST) {
+    const double uc0 = (mid - m[C_]) * ih[C_];
+#pragma unroll
+    for (int j = 0; j < GL8::n / 2; ++j) {
+      const double tau = half * GL8::x(7 - j);
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const double t = side ? tau : -tau;
+        const double uc = fma(t, ih[C_], uc0);
+        const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+        double F[5], g[4];
+#pragma unroll
+        for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
+        integrands(F, g);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < GL8::n; ++j) {
+      const double x = node_x(mid, half, GL8::x(j));
+      const double uc = (x - m[C_]) * ih[C_];
+      const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+      double F[5], g[4];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
+      integrands(F, g);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+    }
+  }
+  range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
+}
+
+// Piece-parallel Epanechnikov stencil.  With one vertex per lane, a warp
+// iterates over the UNION of its lanes' pieces (9 on smooth fields) although a
+// vertex has ~5 non-empty pieces, so ~45 % of the 8-node piece evaluations are
+// idle lanes.  Here each lane first builds its vertex's non-empty pieces; the
+// warp compacts all of them into one list (warp prefix sum) and then evaluates
+// it 32 pieces per round, each lane reading its piece's vertex constants from
+// shared memory.  Per-piece results land in shared memory and every vertex
+// sums its own pieces in piece order, so the result is deterministic and equal
+// to the one-vertex-per-lane kernel's summation order.
+constexpr int kPPWarps = 4;
+constexpr int kPPFields = 18;  // m[5], ih[5], lo[1..4], hi[1..4]
+
+struct PPWarpSmem {
+  double vd[kPPFields][32];  // vertex constants, SoA
+  double pa[9 * 32], pb[9 * 32];
+  double res[9 * 32][4];
+  unsigned char owner[9 * 32];
+  unsigned char fast[32];
+};
+
+__global__ void __launch_bounds__(kPPWarps * 32) closed_epan_pp_kernel(
+    FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
+    double* psad) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  PPWarpSmem& S = reinterpret_cast<PPWarpSmem*>(smem_raw)[warp];
+  const int64_t v = ((int64_t)blockIdx.x * kPPWarps + warp) * 32 + lane;
+  const bool live = v < nvert;
+  int64_t idx = 0;
+  int n = 0;
+  double pts[10];
+  if (live) {
+    const int64_t r = row_begin + v / cols, c = 1 + v % cols;
+    idx = r * f.width + c;
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    double m[5], ih[5], lo[5], hi[5];
+    bool fast = true;
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      double hw;
+      load_epan(f, at[p], m[p], hw);
+      ih[p] = 1.0 / hw;
+      lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
+      hi[p] = m[p] + hw;
+      fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
+    }
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      S.vd[p][lane] = m[p];
+      S.vd[5 + p][lane] = ih[p];
+    }
+#pragma unroll
+    for (int p = 1; p < 5; ++p) {
+      S.vd[9 + p][lane] = lo[p];
+      S.vd[13 + p][lane] = hi[p];
+    }
+    S.fast[lane] = fast ? 1 : 0;
+    double k[8];
+#pragma unroll
+    for (int p = 1; p < 5; ++p) {
+      k[2 * p - 2] = dmin(dmax(lo[p], lo[C_]), hi[C_]);
+      k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
+    }
+    merge_pairs8(k);
+    pts[0] = lo[C_];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pts[q + 1] = k[q];
+    pts[9] = hi[C_];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) n += pts[i + 1] > pts[i] ? 1 : 0;
+  }
+  // warp exclusive prefix sum of the piece counts
+  int off = n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, off, d);
+    if (lane >= d) off += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, off, 31);
+  off -= n;
+  if (live) {
+    int q = off;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (pts[i + 1] > pts[i]) {
+        S.pa[q] = pts[i];
+        S.pb[q] = pts[i + 1];
+        S.owner[q] = (unsigned char)lane;
+        ++q;
+      }
+    }
+  }
+  __syncwarp();
+  for (int e = lane; e < total; e += 32) {
+    const int o = S.owner[e];
+    double m[5], ih[5], lo[5], hi[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      m[p] = S.vd[p][o];
+      ih[p] = S.vd[5 + p][o];
+    }
+#pragma unroll
+    for (int p = 1; p < 5; ++p) {
+      lo[p] = S.vd[9 + p][o];
+      hi[p] = S.vd[13 + p][o];
+    }
+    const double a = S.pa[e], b = S.pb[e];
+    double s[4];
+    bool mk[4];
+    if (S.fast[o]) epan_piece<true>(a, b, m, ih, lo, hi, s, mk);
+    else epan_piece<false>(a, b, m, ih, lo, hi, s, mk);
+    const double half = 0.5 * (b - a);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) S.res[e][r] = mk[r] ? s[r] * half : 0.0;
+  }
+  __syncwarp();
+  if (live) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = off; q < off + n; ++q) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] += S.res[q][r];
+    }
+    store(pmin, pmax, psad, idx, acc);
+  }
+}
+
 // --------------------------------------------------------------- histogram
 // Renormalised weights wn = w / sum(w), cum = [0, cumsum(wn)], binw = (hi-lo)/h;
 // pdf_C = wn[j]/binw, F_P = clip(cum[j] + wn[j] (x - (lo + binw j))/binw, 0, 1)
@@ -837,9 +1016,20 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     case CPB_UNIFORM:
       closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
       break;
-    case CPB_EPANECHNIKOV:
-      closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+    case CPB_EPANECHNIKOV: {
+      static const int pp = [] { const char* e = getenv("CPB_EPAN_PP"); return e ? atoi(e) : 1; }();
+      if (!pp) {
+        closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+        break;
+      }
+      const int64_t cols = f.width - 2, nvert = rows * cols;
+      const int64_t per_block = kPPWarps * 32;
+      const size_t smem = sizeof(PPWarpSmem) * kPPWarps;
+      cudaFuncSetAttribute(closed_epan_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      closed_epan_pp_kernel<<<(unsigned)((nvert + per_block - 1) / per_block), kPPWarps * 32, smem, st>>>(
+          f, row_begin, nvert, cols, pmin, pmax, psad);
       break;
+    }
     case CPB_HISTOGRAM: {
       const size_t tab_smem = ((size_t)4 * (f.bins + 2) + 1) * kTabP * 8;
       static const int variant = [] { const char* e = getenv("CPB_HIST_VARIANT"); return e ? atoi(e) : 0; }();

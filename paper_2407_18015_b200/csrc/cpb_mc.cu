@@ -169,6 +169,100 @@ __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a
   }
 }
 
+// Semianalytical estimator (histogram fields only): engine.py:416-459 and the
+// grid chunk engine.py:669-683.  c centre draws from the keyed stream (plane 0)
+// through the histogram inverse CDF (cum[-1] forced to 1, engine.py:654),
+// each neighbour contributes its exact CDF at the draw (histogram_cdf_values,
+// distributions.py:92-100, with the plain prefix sums), and the conditional
+// pattern probabilities (_conditional_pattern, engine.py:444-459) are averaged.
+// One warp per vertex; lanes accumulate float64 partial sums over a strided
+// subset of the draws and a fixed-shape warp tree adds them, so the result is
+// deterministic (it re-associates numpy's pairwise mean: ~1e-16 relative).
+CPB_D double hist_cdf_at(const double* wn, const double* cum, double lo, double binw, int h,
+                         double x) {
+  double t = floor(__ddiv_rn(__dsub_rn(x, lo), binw));
+  const int j = (int)fmax(0.0, fmin(t, (double)(h - 1)));
+  const double frac = __ddiv_rn(__dsub_rn(x, __dadd_rn(lo, __dmul_rn(binw, (double)j))), binw);
+  const double v = __dadd_rn(cum[j], __dmul_rn(wn[j], frac));
+  return fmin(fmax(v, 0.0), 1.0);
+}
+
+__global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs a) {
+  extern __shared__ double s_tab[];  // per warp: 5 x (h wn + h+1 cum) + 1 x (h+1) centre cum
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int h = f.bins;
+  const int tab = 2 * h + 1;
+  double* my_tab = s_tab + (size_t)warp * (5 * tab + h + 1);
+  double* ccum = my_tab + 5 * tab;  // centre prefix sums with cum[h] = 1 (sampling)
+  const int64_t warps_total = (int64_t)gridDim.x * kMcWarps;
+  for (int64_t v = (int64_t)blockIdx.x * kMcWarps + warp; v < a.nvert; v += warps_total) {
+    const int64_t r = a.row_begin + v / a.cols, c = 1 + v % a.cols;
+    const int64_t idx = r * f.width + c;
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    double lo[5], binw[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      double l, hh;
+      const bool deg = load_bounds(f, at[p], l, hh);
+      lo[p] = l;
+      binw[p] = __ddiv_rn(__dsub_rn(hh, l), (double)h);
+      if (lane == p) {
+        const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at[p]), l, hh, h) : 0;
+        const double total = pairwise_sum([&](int b) { return load_weight(f, at[p], b, deg, dbin); }, h);
+        double* wn = my_tab + p * tab;
+        double* cum = wn + h;
+        double run = 0.0;
+        cum[0] = 0.0;
+        for (int b = 0; b < h; ++b) {
+          wn[b] = __ddiv_rn(load_weight(f, at[p], b, deg, dbin), total);
+          run = __dadd_rn(run, wn[b]);
+          cum[b + 1] = run;
+        }
+        if (p == 0) {
+          for (int b = 0; b <= h; ++b) ccum[b] = cum[b];
+          ccum[h] = 1.0;
+        }
+      }
+    }
+    __syncwarp();
+    Sampler sc;
+    sc.a = lo[0];
+    sc.b = binw[0];
+    sc.wn = my_tab;
+    sc.cum = ccum;
+    const uint64_t px = (uint64_t)((f.row0 + r) * f.gwidth + c);
+    const uint64_t key = plane_key(pixel_key(a.seed, px), 0);
+    double smin = 0.0, smax = 0.0, ssad = 0.0;
+    for (int64_t i = lane; i < a.n; i += 32) {
+      const double x = draw<CPB_HISTOGRAM>(sc, stream_u01(key, (uint64_t)i), 0.0, h);
+      double F[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p)
+        F[p] = hist_cdf_at(my_tab + p * tab, my_tab + p * tab + h, lo[p], binw[p], h, x);
+      const double e = F[1], nn = F[2], w = F[3], s = F[4];
+      smin = __dadd_rn(smin, __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), __dsub_rn(1.0, nn)),
+                                                 __dsub_rn(1.0, w)), __dsub_rn(1.0, s)));
+      smax = __dadd_rn(smax, __dmul_rn(__dmul_rn(__dmul_rn(e, nn), w), s));
+      const double t1 = __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), nn), __dsub_rn(1.0, w)), s);
+      const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(e, __dsub_rn(1.0, nn)), w), __dsub_rn(1.0, s));
+      ssad = __dadd_rn(ssad, __dadd_rn(t1, t2));
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      smin = __dadd_rn(smin, __shfl_xor_sync(0xffffffffu, smin, d));
+      smax = __dadd_rn(smax, __shfl_xor_sync(0xffffffffu, smax, d));
+      ssad = __dadd_rn(ssad, __shfl_xor_sync(0xffffffffu, ssad, d));
+    }
+    if (lane == 0) {
+      const double n = (double)a.n;
+      if (a.pmin) a.pmin[idx] = __ddiv_rn(smin, n);
+      if (a.pmax) a.pmax[idx] = __ddiv_rn(smax, n);
+      if (a.psad) a.psad[idx] = __ddiv_rn(ssad, n);
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void unit_block_kernel(uint64_t seed, const uint64_t* px, int64_t npix, int planes,
                                   int64_t start, int64_t n, double* out) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -238,6 +332,45 @@ int launch_mc(const cpb_field* fld, int64_t row_begin, int64_t row_end, uint64_t
 #undef CPB_MC_KIND
 #undef CPB_MC_LAUNCH
   CPB_CHECK_LAUNCH("monte carlo kernel");
+  return CPB_OK;
+}
+
+int launch_semi(const cpb_field* fld, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t c,
+                double* pmin, double* pmax, double* psad, cudaStream_t st) {
+  const FieldView f = make_view(*fld);
+  const int64_t rows = row_end - row_begin;
+  if (rows <= 0 || f.width < 3) return CPB_OK;
+  if (f.kind != CPB_HISTOGRAM) {
+    set_error("semianalytical estimation is defined for histogram fields only");
+    return CPB_EINVAL;
+  }
+  if (c < 1) {
+    set_error("sample counts must be positive");
+    return CPB_EINVAL;
+  }
+  McArgs a;
+  a.row_begin = row_begin;
+  a.cols = f.width - 2;
+  a.nvert = rows * a.cols;
+  a.seed = seed;
+  a.n = c;
+  a.pmin = pmin;
+  a.pmax = pmax;
+  a.psad = psad;
+  a.counts = nullptr;
+  const size_t smem = (size_t)kMcWarps * (5 * (2 * f.bins + 1) + f.bins + 1) * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_error("too many histogram bins for the semianalytical tables");
+    return CPB_EINVAL;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (a.nvert + kMcWarps - 1) / kMcWarps;
+  const unsigned grid = (unsigned)(want < (int64_t)sms * 64 ? want : (int64_t)sms * 64);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(semi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  semi_kernel<<<grid, kMcWarps * 32, smem, st>>>(f, a);
+  CPB_CHECK_LAUNCH("semianalytical kernel");
   return CPB_OK;
 }
 

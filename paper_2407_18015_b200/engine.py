@@ -9,10 +9,11 @@ Mirrors the grid entry points of critprob.engine
                       as in the reference, never changes the result)
 - ``pixel_index``     engine.py:482-484
 
-Closed form runs ``cpb_classify_closed`` and Monte Carlo runs
-``cpb_classify_mc`` (include/critprob_b200.h).  The semianalytical and
-combinatorial estimators are not on the B200 path yet and raise
-NotImplementedError (they are the "next" rows of SURVEY.md section 8(f)).
+Closed form runs ``cpb_classify_closed``, Monte Carlo ``cpb_classify_mc``
+and the semianalytical estimator ``cpb_classify_semi``
+(include/critprob_b200.h).  The combinatorial estimator (a cross-check
+oracle in the reference, engine.py:320-404) is not on the B200 path yet and
+raises NotImplementedError.
 """
 
 from __future__ import annotations
@@ -98,6 +99,10 @@ def run_rows(dev, estimator: EstimatorSpec, channels, row_begin: int, row_end: i
         _lib.check(lib.cpb_classify_mc(dev.ref(), row_begin, row_end, seed,
                                        int(estimator.n_samples), _lib.RNG_CODES[estimator.rng],
                                        _lib.ptr(pm), _lib.ptr(pM), _lib.ptr(pS), _lib.ptr(counts), s))
+    elif estimator.method == "semianalytical":
+        seed = int(estimator.seed) & ((1 << 64) - 1)
+        _lib.check(lib.cpb_classify_semi(dev.ref(), row_begin, row_end, seed, int(estimator.c),
+                                         _lib.ptr(pm), _lib.ptr(pM), _lib.ptr(pS), s))
     else:
         raise NotImplementedError(
             f"the {estimator.method} estimator is not on the B200 path yet")
@@ -123,9 +128,8 @@ def classify_field(
 
     estimator = estimator or EstimatorSpec()
     channels = _validate(field, estimator, workers, channels)
-    if estimator.method in ("semianalytical", "combinatorial"):
-        raise NotImplementedError(
-            f"the {estimator.method} estimator is not on the B200 path yet")
+    if estimator.method == "combinatorial":
+        raise NotImplementedError("the combinatorial estimator is not on the B200 path yet")
     dev = field.device_field()
     H, W = field.shape
     planes = torch.zeros((3, H, W), dtype=torch.float64, device=dev.device)

@@ -19,4 +19,4 @@ def golden():
     import numpy as np
 
     return {name: dict(np.load(os.path.join(GOLDEN, name + ".npz")))
-            for name in ("fit", "closed", "mc", "rng")}
+            for name in ("fit", "closed", "mc", "rng", "semi")}

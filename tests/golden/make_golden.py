@@ -13,6 +13,7 @@ The fixtures travel with the repo; nothing at test time reads
 - UncertainField.from_scalar    (fields.py:160-178)
 - classify_field closed form    (engine.py:716-787, 594-629)
 - classify_field Monte Carlo    (engine.py:659-666, 632-656)
+- classify_field semianalytical (engine.py:669-683)
 - rngstream.unit_block          (rngstream.py:33-48)
 """
 
@@ -76,6 +77,7 @@ def main() -> None:
     fit = {}
     closed = {}
     mc = {}
+    semi = {}
     for name, vals in ens.items():
         fit[f"ens/{name}"] = vals
         stack = EnsembleStack(vals)
@@ -99,6 +101,12 @@ def main() -> None:
                 for ch in ("min", "max", "saddle"):
                     mc[f"{tag}/{ch}"] = prob.channel(ch)
                 mc[f"{tag}/n"] = np.array(n)
+            if kind == "histogram" and name in ("ackley", "rand", "degenerate") and bins in (3, 5, 9):
+                est = EstimatorSpec(method="semianalytical", c=700, seed=2)
+                prob = classify_field(field, est)
+                for ch in ("min", "max", "saddle"):
+                    semi[f"{tag}/{ch}"] = prob.channel(ch)
+                semi[f"{tag}/c"] = np.array(700)
 
     # closed-form known answers on hand-built 3x3 uniform fields (test_engine.py:147-163)
     lo = np.zeros((3, 3))
@@ -136,7 +144,8 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "closed.npz"), **closed)
     np.savez_compressed(os.path.join(HERE, "mc.npz"), **mc)
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **rng_fx)
-    for f in ("fit", "closed", "mc", "rng"):
+    np.savez_compressed(os.path.join(HERE, "semi.npz"), **semi)
+    for f in ("fit", "closed", "mc", "rng", "semi"):
         print(f, os.path.getsize(os.path.join(HERE, f + ".npz")), "bytes")
 
 

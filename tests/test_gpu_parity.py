@@ -310,3 +310,41 @@ def test_synthetic_rows_match_host_twin():
     assert np.array_equal(dev, host)
     part = cpb.synthetic_rows(13, 5, 33, 40, 7, seed=4).cpu().numpy()
     assert np.array_equal(part, host[:, 13:18])
+
+
+# ---------------------------------------------------------------- semianalytical
+SEMI_TOL = 1e-13  # per-draw arithmetic is numpy's; only the mean's summation order differs
+
+
+def test_semianalytical_against_reference(golden):
+    fit, semi = golden["fit"], golden["semi"]
+    seen = 0
+    for key in semi:
+        parts = key.split("/")
+        if len(parts) != 4 or parts[3] != "c":
+            continue
+        name, kind, bins = parts[0], parts[1], int(parts[2])
+        c = int(semi[key])
+        prob = cpb.classify_field(_fit(fit[f"ens/{name}"], kind, bins),
+                                  cpb.EstimatorSpec(method="semianalytical", c=c, seed=2))
+        for ch in ("min", "max", "saddle"):
+            err = np.max(np.abs(prob.channel(ch) - semi[f"{name}/{kind}/{bins}/{ch}"]))
+            assert err <= SEMI_TOL, (key, ch, err)
+        seen += 1
+    assert seen >= 6
+
+
+def test_semianalytical_close_to_closed_form():
+    # test_acceptance.py:185-216: RMSE < 0.01 against the closed form
+    vals = orc.ackley_ensemble(40, 36, 20, noise_amp=0.3, seed=2)
+    field = _fit(vals, "histogram", 5)
+    closed = cpb.classify_field(field)
+    semi = cpb.classify_field(field, cpb.EstimatorSpec(method="semianalytical", c=10000, seed=0))
+    ref = orc.classify(orc.fit(vals, "histogram", 5), "histogram", method="semianalytical",
+                       n_samples=10000, seed=0)
+    for ch in ("min", "max", "saddle"):
+        d = semi.channel(ch)[1:-1, 1:-1] - closed.channel(ch)[1:-1, 1:-1]
+        assert np.sqrt(np.mean(d * d)) < 0.01
+        assert np.max(np.abs(semi.channel(ch) - ref[ch])) <= SEMI_TOL
+    with pytest.raises(ValueError):
+        cpb.classify_field(_fit(vals, "uniform"), cpb.EstimatorSpec(method="semianalytical"))

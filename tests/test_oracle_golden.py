@@ -132,3 +132,20 @@ def test_synthetic_rows_consistent():
     part = orc.synthetic_rows(5, 4, 10, 12, 6)
     assert full.dtype == np.float32 and full.shape == (6, 12, 10)
     assert np.array_equal(full[:, 5:9], part)
+
+
+def test_semianalytical_bitexact(golden):
+    fit, semi = golden["fit"], golden["semi"]
+    seen = 0
+    for key in semi:
+        parts = key.split("/")
+        if len(parts) != 4 or parts[3] != "c":
+            continue
+        name, kind, bins = parts[0], parts[1], int(parts[2])
+        c = int(semi[key])
+        params = orc.fit(fit[f"ens/{name}"], kind, bins=bins)
+        got = orc.classify(params, kind, method="semianalytical", n_samples=c, seed=2)
+        for ch in ("min", "max", "saddle"):
+            assert np.array_equal(got[ch], semi[f"{name}/{kind}/{bins}/{ch}"]), (key, ch)
+        seen += 1
+    assert seen >= 6
