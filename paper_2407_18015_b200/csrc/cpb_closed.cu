@@ -204,6 +204,52 @@ CPB_D void uniform_pieces(const double* lo, const double* hi, const double* inv,
   }
 }
 
+// One uniform piece [a, b]: s[r] = GL3 sum of integrand r (before half, pdf).
+template <bool FAST>
+CPB_D void uniform_piece(double a, double b, const double* lo, const double* hi, const double* inv,
+                         double s[4], bool mk[4]) {
+  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+  bool bl[5], ab[5];
+  double al[5], be[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
+    const bool in = !(bl[p] | ab[p]);
+    be[p] = in ? inv[p] : 0.0;
+    al[p] = in ? (FAST ? (mid - lo[p]) * inv[p] : 0.0) : (ab[p] ? 1.0 : 0.0);
+  }
+  double F[5], g[4];
+  if (FAST) {
+    const double tau = half * GL3::x(2);
+#pragma unroll
+    for (int p = 1; p < 5; ++p) F[p] = al[p];
+    integrands(F, g);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s[r] = GL3::w(1) * g[r];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+#pragma unroll
+      for (int p = 1; p < 5; ++p) F[p] = fma(side ? tau : -tau, be[p], al[p]);
+      integrands(F, g);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(0), g[r], s[r]);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s[r] = 0.0;
+#pragma unroll
+    for (int j = 0; j < GL3::n; ++j) {
+      const double x = node_x(mid, half, GL3::x(j));
+#pragma unroll
+      for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
+      integrands(F, g);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
+    }
+  }
+  range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
+}
+
 __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
     FieldView f, Window w, double* pmin, double* pmax, double* psad) {
   int64_t idx;
@@ -402,7 +448,10 @@ struct PPWarpSmem {
   unsigned char fast[32];
 };
 
-__global__ void __launch_bounds__(kPPWarps * 32) closed_epan_pp_kernel(
+// KIND = CPB_UNIFORM (vertex constants lo[5], hi[5], inv[5]) or
+// CPB_EPANECHNIKOV (m[5], ih[5], lo[1..4], hi[1..4]).
+template <int KIND>
+__global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
     double* psad) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -417,26 +466,39 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_pp_kernel(
     const int64_t r = row_begin + v / cols, c = 1 + v % cols;
     idx = r * f.width + c;
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
-    double m[5], ih[5], lo[5], hi[5];
+    double lo[5], hi[5];
     bool fast = true;
+    if (KIND == CPB_UNIFORM) {
 #pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      double hw;
-      load_epan(f, at[p], m[p], hw);
-      ih[p] = 1.0 / hw;
-      lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
-      hi[p] = m[p] + hw;
-      fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
-    }
+      for (int p = 0; p < 5; ++p) {
+        load_bounds(f, at[p], lo[p], hi[p]);
+        const double inv = 1.0 / (hi[p] - lo[p]);
+        fast &= (fabs(lo[p]) + fabs(hi[p])) * inv <= kFastRatio;
+        S.vd[p][lane] = lo[p];
+        S.vd[5 + p][lane] = hi[p];
+        S.vd[10 + p][lane] = inv;
+      }
+    } else {
+      double m[5], ih[5];
 #pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      S.vd[p][lane] = m[p];
-      S.vd[5 + p][lane] = ih[p];
-    }
+      for (int p = 0; p < 5; ++p) {
+        double hw;
+        load_epan(f, at[p], m[p], hw);
+        ih[p] = 1.0 / hw;
+        lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
+        hi[p] = m[p] + hw;
+        fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
+      }
 #pragma unroll
-    for (int p = 1; p < 5; ++p) {
-      S.vd[9 + p][lane] = lo[p];
-      S.vd[13 + p][lane] = hi[p];
+      for (int p = 0; p < 5; ++p) {
+        S.vd[p][lane] = m[p];
+        S.vd[5 + p][lane] = ih[p];
+      }
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        S.vd[9 + p][lane] = lo[p];
+        S.vd[13 + p][lane] = hi[p];
+      }
     }
     S.fast[lane] = fast ? 1 : 0;
     double k[8];
@@ -477,22 +539,34 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_pp_kernel(
   __syncwarp();
   for (int e = lane; e < total; e += 32) {
     const int o = S.owner[e];
-    double m[5], ih[5], lo[5], hi[5];
-#pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      m[p] = S.vd[p][o];
-      ih[p] = S.vd[5 + p][o];
-    }
-#pragma unroll
-    for (int p = 1; p < 5; ++p) {
-      lo[p] = S.vd[9 + p][o];
-      hi[p] = S.vd[13 + p][o];
-    }
     const double a = S.pa[e], b = S.pb[e];
     double s[4];
     bool mk[4];
-    if (S.fast[o]) epan_piece<true>(a, b, m, ih, lo, hi, s, mk);
-    else epan_piece<false>(a, b, m, ih, lo, hi, s, mk);
+    if (KIND == CPB_UNIFORM) {
+      double lo[5], hi[5], inv[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        lo[p] = S.vd[p][o];
+        hi[p] = S.vd[5 + p][o];
+        inv[p] = S.vd[10 + p][o];
+      }
+      if (S.fast[o]) uniform_piece<true>(a, b, lo, hi, inv, s, mk);
+      else uniform_piece<false>(a, b, lo, hi, inv, s, mk);
+    } else {
+      double m[5], ih[5], lo[5], hi[5];
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        m[p] = S.vd[p][o];
+        ih[p] = S.vd[5 + p][o];
+      }
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        lo[p] = S.vd[9 + p][o];
+        hi[p] = S.vd[13 + p][o];
+      }
+      if (S.fast[o]) epan_piece<true>(a, b, m, ih, lo, hi, s, mk);
+      else epan_piece<false>(a, b, m, ih, lo, hi, s, mk);
+    }
     const double half = 0.5 * (b - a);
 #pragma unroll
     for (int r = 0; r < 4; ++r) S.res[e][r] = mk[r] ? s[r] * half : 0.0;
@@ -503,6 +577,11 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_pp_kernel(
     for (int q = off; q < off + n; ++q) {
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[r] += S.res[q][r];
+    }
+    if (KIND == CPB_UNIFORM) {
+      const double pdf = S.vd[10][lane];  // 1 / (hi_C - lo_C)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] *= pdf;
     }
     store(pmin, pmax, psad, idx, acc);
   }
@@ -1012,21 +1091,30 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     set_error("grid too large for one launch (%lld blocks)", (long long)blocks);
     return CPB_EINVAL;
   }
+  // CPB_PP=0 selects the one-vertex-per-lane kernels (A/B experiments)
+  static const int pp = [] { const char* e = getenv("CPB_PP"); return e ? atoi(e) : 1; }();
+  const int64_t cols = f.width - 2, nvert = rows * cols;
+  const int64_t pp_blocks = (nvert + kPPWarps * 32 - 1) / (kPPWarps * 32);
+  const size_t pp_smem = sizeof(PPWarpSmem) * kPPWarps;
   switch (f.kind) {
     case CPB_UNIFORM:
-      closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+      // 3-node pieces are too cheap to amortise the redistribution (measured
+      // 18.6 ms per-lane vs 25.4 ms piece-parallel at 16384^2): per-lane by default
+      if (pp != 2) {
+        closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+        break;
+      }
+      cudaFuncSetAttribute(closed_pp_kernel<CPB_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
+      closed_pp_kernel<CPB_UNIFORM><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
+          f, row_begin, nvert, cols, pmin, pmax, psad);
       break;
     case CPB_EPANECHNIKOV: {
-      static const int pp = [] { const char* e = getenv("CPB_EPAN_PP"); return e ? atoi(e) : 1; }();
       if (!pp) {
         closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
         break;
       }
-      const int64_t cols = f.width - 2, nvert = rows * cols;
-      const int64_t per_block = kPPWarps * 32;
-      const size_t smem = sizeof(PPWarpSmem) * kPPWarps;
-      cudaFuncSetAttribute(closed_epan_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      closed_epan_pp_kernel<<<(unsigned)((nvert + per_block - 1) / per_block), kPPWarps * 32, smem, st>>>(
+      cudaFuncSetAttribute(closed_pp_kernel<CPB_EPANECHNIKOV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
+      closed_pp_kernel<CPB_EPANECHNIKOV><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
           f, row_begin, nvert, cols, pmin, pmax, psad);
       break;
     }
