@@ -448,6 +448,219 @@ struct PPWarpSmem {
   unsigned char fast[32];
 };
 
+struct PPAdaSmem : PPWarpSmem {
+  unsigned short slot[9 * 32];  // result slot of a (class-sorted) piece
+};
+
+// Degree-adaptive fast-mode Epanechnikov piece: NN symmetric GL nodes (exact
+// for the piece's integrand degree 2 + 3k, see GLSym).
+template <int NN>
+CPB_D void epan_piece_fast_n(double a, double b, const double* m, const double* ih,
+                             const double* lo, const double* hi, double s[4], bool mk[4]) {
+  const double pdf0 = 0.75 * ih[C_];
+  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+  bool bl[5], ab[5];
+  double al[5], be[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
+    const bool in = !(bl[p] | ab[p]);
+    be[p] = in ? ih[p] : 0.0;
+    al[p] = in ? (mid - m[p]) * ih[p] : (ab[p] ? 1.0 : -1.0);
+  }
+  const double uc0 = (mid - m[C_]) * ih[C_];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) s[r] = 0.0;
+  if (NN & 1) {  // centre node
+    const double wp = GLSym<NN>::w0() * (pdf0 * fma(-uc0, uc0, 1.0));
+    double F[5], g[4];
+#pragma unroll
+    for (int p = 1; p < 5; ++p) F[p] = epan_cdf(al[p]);
+    integrands(F, g);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+  }
+#pragma unroll
+  for (int j = 0; j < GLSym<NN>::pairs; ++j) {
+    const double tau = half * GLSym<NN>::x(j);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const double t = side ? tau : -tau;
+      const double uc = fma(t, ih[C_], uc0);
+      const double wp = GLSym<NN>::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+      double F[5], g[4];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
+      integrands(F, g);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+    }
+  }
+  range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
+}
+
+// Piece-parallel AND degree-adaptive Epanechnikov stencil.  On a piece where
+// only k of the four neighbour CDFs are non-constant the integrands have
+// degree 2 + 3k, so 2, 3, 5, 6 or 8 Gauss-Legendre nodes are exact (the
+// reference always uses 8, engine.py:600-601; the difference is rounding).
+// The warp sorts its compacted piece list by k (counting sort with warp
+// scans) and evaluates class by class, so every round runs one node count on
+// all 32 lanes.  Pieces of exact-mode vertices keep the 8-node exact path.
+__global__ void __launch_bounds__(kPPWarps * 32) closed_epan_ada_kernel(
+    FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
+    double* psad) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  PPAdaSmem& S = reinterpret_cast<PPAdaSmem*>(smem_raw)[warp];
+  const int64_t v = ((int64_t)blockIdx.x * kPPWarps + warp) * 32 + lane;
+  const bool live = v < nvert;
+  int64_t idx = 0;
+  int n = 0;
+  double pts[10];
+  double lo[5], hi[5];
+  bool fast = true;
+  if (live) {
+    const int64_t r = row_begin + v / cols, c = 1 + v % cols;
+    idx = r * f.width + c;
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    double m[5], ih[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      double hw;
+      load_epan(f, at[p], m[p], hw);
+      ih[p] = 1.0 / hw;
+      lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
+      hi[p] = m[p] + hw;
+      fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
+    }
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      S.vd[p][lane] = m[p];
+      S.vd[5 + p][lane] = ih[p];
+    }
+#pragma unroll
+    for (int p = 1; p < 5; ++p) {
+      S.vd[9 + p][lane] = lo[p];
+      S.vd[13 + p][lane] = hi[p];
+    }
+    S.fast[lane] = fast ? 1 : 0;
+    double k[8];
+#pragma unroll
+    for (int p = 1; p < 5; ++p) {
+      k[2 * p - 2] = dmin(dmax(lo[p], lo[C_]), hi[C_]);
+      k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
+    }
+    merge_pairs8(k);
+    pts[0] = lo[C_];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pts[q + 1] = k[q];
+    pts[9] = hi[C_];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) n += pts[i + 1] > pts[i] ? 1 : 0;
+  }
+  // class of a piece: number of neighbours inside their support (5 = exact mode)
+  auto piece_class = [&](double a, double b) {
+    if (!fast) return 5;
+    const double mid = 0.5 * (b + a);
+    int kk = 0;
+#pragma unroll
+    for (int p = 1; p < 5; ++p) kk += (mid > lo[p] && mid < hi[p]) ? 1 : 0;
+    return kk;
+  };
+  int cnt[6] = {0, 0, 0, 0, 0, 0};
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (pts[i + 1] > pts[i]) {
+        const int cl = piece_class(pts[i], pts[i + 1]);
+#pragma unroll
+        for (int q = 0; q < 6; ++q) cnt[q] += q == cl ? 1 : 0;
+      }
+    }
+  }
+  // warp scans: slot offsets (original order) and class-sorted positions
+  int off = n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, off, d);
+    if (lane >= d) off += y;
+  }
+  off -= n;
+  int pos[6], base = 0, ctot[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    int x = cnt[q];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    ctot[q] = __shfl_sync(0xffffffffu, x, 31);
+    pos[q] = base + x - cnt[q];
+    base += ctot[q];
+  }
+  if (live) {
+    int j = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (pts[i + 1] > pts[i]) {
+        const int cl = piece_class(pts[i], pts[i + 1]);
+        int e = 0;
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          if (q == cl) e = pos[q]++;
+        S.pa[e] = pts[i];
+        S.pb[e] = pts[i + 1];
+        S.owner[e] = (unsigned char)lane;
+        S.slot[e] = (unsigned short)(off + j);
+        ++j;
+      }
+    }
+  }
+  __syncwarp();
+  int cbase = 0;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    for (int e = cbase + lane; e < cbase + ctot[q]; e += 32) {
+      const int o = S.owner[e];
+      double m[5], ih[5], plo[5], phi[5];
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        m[p] = S.vd[p][o];
+        ih[p] = S.vd[5 + p][o];
+      }
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        plo[p] = S.vd[9 + p][o];
+        phi[p] = S.vd[13 + p][o];
+      }
+      const double a = S.pa[e], b = S.pb[e];
+      double s[4];
+      bool mk[4];
+      if (q == 0) epan_piece_fast_n<2>(a, b, m, ih, plo, phi, s, mk);
+      else if (q == 1) epan_piece_fast_n<3>(a, b, m, ih, plo, phi, s, mk);
+      else if (q == 2) epan_piece_fast_n<5>(a, b, m, ih, plo, phi, s, mk);
+      else if (q == 3) epan_piece_fast_n<6>(a, b, m, ih, plo, phi, s, mk);
+      else if (q == 4) epan_piece_fast_n<8>(a, b, m, ih, plo, phi, s, mk);
+      else epan_piece<false>(a, b, m, ih, plo, phi, s, mk);
+      const double half = 0.5 * (b - a);
+      const int sl = S.slot[e];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) S.res[sl][r] = mk[r] ? s[r] * half : 0.0;
+    }
+    cbase += ctot[q];
+  }
+  __syncwarp();
+  if (live) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int q = off; q < off + n; ++q) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] += S.res[q][r];
+    }
+    store(pmin, pmax, psad, idx, acc);
+  }
+}
+
 // KIND = CPB_UNIFORM (vertex constants lo[5], hi[5], inv[5]) or
 // CPB_EPANECHNIKOV (m[5], ih[5], lo[1..4], hi[1..4]).
 template <int KIND>
@@ -1111,6 +1324,14 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     case CPB_EPANECHNIKOV: {
       if (!pp) {
         closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+        break;
+      }
+      if (pp == 3) {  // piece-parallel + degree-adaptive node counts (per-warp classes:
+                      // the per-class round padding ate the saving, 59.6 vs 38 ms; kept for A/B)
+        const size_t ada_smem = sizeof(PPAdaSmem) * kPPWarps;
+        cudaFuncSetAttribute(closed_epan_ada_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ada_smem);
+        closed_epan_ada_kernel<<<(unsigned)pp_blocks, kPPWarps * 32, ada_smem, st>>>(
+            f, row_begin, nvert, cols, pmin, pmax, psad);
         break;
       }
       cudaFuncSetAttribute(closed_pp_kernel<CPB_EPANECHNIKOV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);

@@ -39,6 +39,59 @@ struct GL3 {
   CPB_HD static double w(int i) { return i == 1 ? 0x1.c71c71c71c71cp-1 : 0x1.1c71c71c71c73p-1; }
 };
 
+// Symmetric Gauss-Legendre rules by node count, as (positive node, weight)
+// pairs plus the centre weight for odd counts -- numpy leggauss(n) bits.
+// Used by the degree-adaptive Epanechnikov stencil: a piece whose integrand
+// has degree 2 + 3k (k neighbours inside their support) is integrated exactly
+// by n = 2, 3, 5, 6, 8 nodes for k = 0..4.
+template <int NN>
+struct GLSym;
+template <>
+struct GLSym<2> {
+  static constexpr int pairs = 2 / 2;
+  CPB_HD static double x(int) { return 0x1.279a74590331cp-1; }
+  CPB_HD static double w(int) { return 0x1.0000000000000p+0; }
+  CPB_HD static double w0() { return 0.0; }
+};
+template <>
+struct GLSym<3> {
+  static constexpr int pairs = 1;
+  CPB_HD static double x(int) { return 0x1.8c97ef43f7248p-1; }
+  CPB_HD static double w(int) { return 0x1.1c71c71c71c73p-1; }
+  CPB_HD static double w0() { return 0x1.c71c71c71c71cp-1; }
+};
+template <>
+struct GLSym<5> {
+  static constexpr int pairs = 2;
+  CPB_HD static double x(int i) { return i == 0 ? 0x1.cff6ce0533a69p-1 : 0x1.13b23fd99b705p-1; }
+  CPB_HD static double w(int i) { return i == 0 ? 0x1.e539ec36e0393p-3 : 0x1.ea1da25ae4158p-2; }
+  CPB_HD static double w0() { return 0x1.23456789abcddp-1; }
+};
+template <>
+struct GLSym<6> {
+  static constexpr int pairs = 3;
+  CPB_HD static double x(int i) {
+    return i == 0 ? 0x1.dd6ca4e80a01dp-1 : (i == 1 ? 0x1.528a09655c95ep-1 : 0x1.e8b12d03675c5p-3);
+  }
+  CPB_HD static double w(int i) {
+    return i == 0 ? 0x1.5edf601e2dbf5p-3 : (i == 1 ? 0x1.716b7b5794c1ep-2 : 0x1.df24d499545e8p-2);
+  }
+  CPB_HD static double w0() { return 0.0; }
+};
+template <>
+struct GLSym<8> {
+  static constexpr int pairs = 4;
+  CPB_HD static double x(int i) {
+    return i == 0 ? 0x1.ebab1cb0acc66p-1
+                  : (i == 1 ? 0x1.97e4ab249f41ep-1 : (i == 2 ? 0x1.0d129583284b4p-1 : 0x1.77ac94f3c7344p-3));
+  }
+  CPB_HD static double w(int i) {
+    return i == 0 ? 0x1.9ea1d04ca03aep-4
+                  : (i == 1 ? 0x1.c76fb531d2b94p-3 : (i == 2 ? 0x1.413c50a25560ep-2 : 0x1.736360b19933dp-2));
+  }
+  CPB_HD static double w0() { return 0.0; }
+};
+
 struct GL8 {
   static constexpr int n = 8;
   CPB_HD static double x(int i) {
