@@ -236,6 +236,118 @@ CPB_D float bin_threshold(int k, double lo, double scale) {
 
 // NT: histogram bin count handled with NT-1 register thresholds (1..kThreshBins),
 // or 0 for the shared-memory counters (more bins).
+// Histogram fit with two threads per pixel (the bin counts and min/max are
+// order-free, unlike the Epanechnikov sums): thread halves take members
+// [0, M/2) and [M/2, M) of the staged tile, exchange min/max through shared
+// memory, both derive the same exact thresholds, count their halves and add.
+// Twice the warps per SM of fit_tma_kernel for the compare-heavy binning.
+template <int NT>
+__global__ void __launch_bounds__(2 * kTmaTile) fit_tma_hist2_kernel(
+    const __grid_constant__ CUtensorMap map, FitArgs a, int stages, int mbox, int nbox,
+    int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  static_assert(NT >= 1, "threshold path only");
+  const int M = a.members, h = a.bins;
+  const int rows = mbox * nbox;
+  const int tid = threadIdx.x, px = tid % kTmaTile, half = tid / kTmaTile;
+  const int m0 = half ? M / 2 : 0, m1 = half ? M : M / 2;
+  float* buf = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * rows * kTmaTile * 4);
+  float* xlo = reinterpret_cast<float*>(full + stages);  // [2][kTmaTile]
+  float* xhi = xlo + 2 * kTmaTile;
+  uint32_t* xc = reinterpret_cast<uint32_t*>(xhi + 2 * kTmaTile);  // [NT][kTmaTile] from half 1
+  if (tid == 0) {
+    prefetch_tensormap(&map);
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const uint32_t tile_bytes = (uint32_t)rows * kTmaTile * 4u;
+  auto issue = [&](int64_t tile, int s) {
+    mbar_arrive_expect_tx(&full[s], tile_bytes);
+    float* dst = buf + (size_t)s * rows * kTmaTile;
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(dst + (size_t)b * mbox * kTmaTile, &map, (int)(tile * kTmaTile), b * mbox, &full[s], pol);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < stages; ++k) {
+      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+      if (t < ntiles) issue(t, k);
+    }
+  }
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % stages;
+    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+    const float* col = buf + (size_t)s * rows * kTmaTile + px;
+    const int64_t p = t * kTmaTile + px;
+    const bool live = p < a.npix;
+    float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+    if (live) {
+#pragma unroll 8
+      for (int m = m0; m < m1; ++m) {
+        const float x = col[m * kTmaTile];
+        bad |= nonfinite(x);
+        lo = fminf(lo, x);
+        hi = fmaxf(hi, x);
+      }
+    }
+    xlo[half * kTmaTile + px] = lo;
+    xhi[half * kTmaTile + px] = hi;
+    __syncthreads();
+    lo = fminf(xlo[px], xlo[kTmaTile + px]);
+    hi = fmaxf(xhi[px], xhi[kTmaTile + px]);
+    vmin = fminf(vmin, lo);
+    vmax = fmaxf(vmax, hi);
+    uint32_t c[NT + 1];
+#pragma unroll
+    for (int q = 0; q <= NT; ++q) c[q] = 0u;
+    const bool flat = !(hi > lo);
+    if (live && !flat) {
+      const double dlo = (double)lo;
+      const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
+      float thr[NT];
+#pragma unroll
+      for (int q = 1; q < NT; ++q) thr[q] = bin_threshold(q, dlo, scale);
+#pragma unroll 4
+      for (int m = m0; m < m1; ++m) {
+        const float x = col[m * kTmaTile];
+#pragma unroll
+        for (int q = 1; q < NT; ++q) c[q] += (x >= thr[q]) ? 1u : 0u;
+      }
+    }
+    if (half) {
+#pragma unroll
+      for (int q = 1; q < NT; ++q) xc[q * kTmaTile + px] = c[q];
+    }
+    __syncthreads();
+    if (!half && live) {
+#pragma unroll
+      for (int q = 1; q < NT; ++q) c[q] += xc[q * kTmaTile + px];
+      c[0] = (uint32_t)M;
+      a.lo[p] = lo;
+      a.hi[p] = hi;
+#pragma unroll
+      for (int b = 0; b < NT; ++b) {
+        const uint32_t v = flat ? 0u : (b + 1 < NT ? c[b] - c[b + 1] : c[b]);
+        if (a.wmode == CPB_WEIGHTS_U8)
+          static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
+        else
+          static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
+      }
+    }
+    __syncthreads();  // every thread is done with stage s and the exchange buffers
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)stages * gridDim.x;
+      if (tn < ntiles) issue(tn, s);
+    }
+  }
+  merge_range(vmin, vmax, bad, a.range);
+}
+
 template <int KIND, int NT>
 __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                            FitArgs a, int stages, int mbox,
@@ -542,15 +654,38 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
     kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);            \
   } while (0)
+#define CPB_FIT_TMA_SPLIT(KERN)                                                                  \
+  do {                                                                                           \
+    auto kern = KERN;                                                                            \
+    const size_t sm2 = stages * tile_bytes + stages * 8 + (4 + kThreshBins) * kTmaTile * 4;      \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);           \
+    int per_sm = 1;                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * kTmaTile, sm2);             \
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
+    kern<<<(unsigned)grid, 2 * kTmaTile, sm2, st>>>(map, c, stages, mbox, nbox, ntiles);         \
+  } while (0)
 #define CPB_FIT_TMA(K) \
   case K:              \
     CPB_FIT_TMA_LAUNCH((fit_tma_kernel<K, 0>)); \
     break;
+      static const int split = [] { const char* e = getenv("CPB_HIST_SPLIT"); return e ? atoi(e) : 0; }();
       switch (f->kind) {
         CPB_FIT_TMA(CPB_UNIFORM)
         CPB_FIT_TMA(CPB_EPANECHNIKOV)
         CPB_FIT_TMA(CPB_GAUSSIAN)
         case CPB_HISTOGRAM:
+          if (split && f->bins >= 2 && f->bins <= kThreshBins) {
+            switch (f->bins) {
+              case 2: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<2>)); break;
+              case 3: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<3>)); break;
+              case 4: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<4>)); break;
+              case 5: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<5>)); break;
+              case 6: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<6>)); break;
+              case 7: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<7>)); break;
+              default: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<8>)); break;
+            }
+            break;
+          }
           switch (f->bins <= kThreshBins ? f->bins : 0) {
             case 1: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 1>)); break;
             case 2: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 2>)); break;
@@ -568,6 +703,7 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
           return CPB_EINVAL;
       }
 #undef CPB_FIT_TMA_LAUNCH
+#undef CPB_FIT_TMA_SPLIT
 #undef CPB_FIT_TMA
       CPB_CHECK_LAUNCH("fit kernel (TMA)");
     }

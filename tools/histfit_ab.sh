@@ -1,0 +1,3 @@
+python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+for v in 0 1; do CPB_HIST_SPLIT=$v python bench.py --no-e2e --steps 2 --warmup 2 --models histogram --serial > gpurun_out/hf_v$v.log 2>&1; echo "split=$v"; python -c "
+import json; d=json.loads(open('gpurun_out/hf_v$v.log').read().strip().splitlines()[-1]); print(json.dumps(d['roofline']['kernels']), d['parity'])"; done
