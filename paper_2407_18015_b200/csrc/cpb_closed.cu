@@ -1117,6 +1117,20 @@ __global__ void __launch_bounds__(kHistThreads, MINB) closed_hist_smem_kernel(
 constexpr int kTabTW = 32, kTabTH = 8, kTabMaxBins = 16;
 constexpr int kTabSW = kTabTW + 2, kTabP = kTabSW * (kTabTH + 2);
 
+// numpy pairwise summation of exactly N <= 8 terms (sequential below 8, one
+// 8-accumulator tree at 8)
+template <int N>
+CPB_D double pairwise_small(const double* w) {
+  if (N < 8) {
+    double r = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) r = __dadd_rn(r, w[i]);
+    return r;
+  }
+  return __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1 % N]), __dadd_rn(w[2 % N], w[3 % N])),
+                   __dadd_rn(__dadd_rn(w[4 % N], w[5 % N]), __dadd_rn(w[6 % N], w[7 % N])));
+}
+
 // numpy pairwise summation of w[0..n) for n <= 16 (register array, unrolled)
 CPB_D double pairwise16(const double* w, int n) {
   if (n < 8) {
@@ -1141,12 +1155,15 @@ CPB_D double pairwise16(const double* w, int n) {
   return res;
 }
 
+// HB: bin count when <= 8 (compile-time: exact-size staging loops), else 16
+// (runtime bins 9..16).
+template <int HB>
 __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     FieldView f, int64_t row_begin, int64_t row_end, int ctiles, double* pmin, double* pmax,
     double* psad) {
   extern __shared__ double sm[];
   constexpr int P = kTabP, SW = kTabSW;
-  const int h = f.bins;
+  const int h = HB <= 8 ? HB : f.bins;
   double* T = sm;                          // [(h + 2) states][4 fields][P pixels]
   double* RATIO = sm + (size_t)(h + 2) * 4 * P;  // (|lo| + |hi|) / binw, fast-mode test
   const int64_t r0 = row_begin + (int64_t)(blockIdx.x / ctiles) * kTabTH;
@@ -1161,9 +1178,9 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     double lo, hi;
     const bool deg = load_bounds(f, at, lo, hi);
     const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at), lo, hi, h) : 0;
-    double wv[kTabMaxBins];
+    double wv[HB];
 #pragma unroll
-    for (int b = 0; b < kTabMaxBins; ++b) {
+    for (int b = 0; b < HB; ++b) {
       double wb = 0.0;
       if (b < h) {
         if (f.wmode == CPB_WEIGHTS_F64) {
@@ -1179,12 +1196,12 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
       }
       wv[b] = wb;
     }
-    const double it = 1.0 / pairwise16(wv, h);
+    const double it = 1.0 / (HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
     T[0 * P + i] = 0.0; T[1 * P + i] = 0.0; T[2 * P + i] = 0.0; T[3 * P + i] = lo;
     double cum = 0.0;
 #pragma unroll
-    for (int b = 0; b < kTabMaxBins; ++b) {
+    for (int b = 0; b < HB; ++b) {
       if (b < h) {
         const double wn = wv[b] * it;
         double* t = T + (size_t)(b + 1) * 4 * P + i;
@@ -1347,8 +1364,20 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       if (variant == 0 && f.bins <= kTabMaxBins && tab_smem <= 200 * 1024) {
         const int ctiles = (int)((f.width - 2 + kTabTW - 1) / kTabTW);
         const int64_t rtiles = (rows + kTabTH - 1) / kTabTH;
-        cudaFuncSetAttribute(closed_hist_tab_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem);
-        closed_hist_tab_kernel<<<(unsigned)(rtiles * ctiles), dim3(kTabTW, kTabTH), tab_smem, st>>>(
+        auto kern = closed_hist_tab_kernel<16>;
+        switch (f.bins) {
+          case 1: kern = closed_hist_tab_kernel<1>; break;
+          case 2: kern = closed_hist_tab_kernel<2>; break;
+          case 3: kern = closed_hist_tab_kernel<3>; break;
+          case 4: kern = closed_hist_tab_kernel<4>; break;
+          case 5: kern = closed_hist_tab_kernel<5>; break;
+          case 6: kern = closed_hist_tab_kernel<6>; break;
+          case 7: kern = closed_hist_tab_kernel<7>; break;
+          case 8: kern = closed_hist_tab_kernel<8>; break;
+          default: break;
+        }
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem);
+        kern<<<(unsigned)(rtiles * ctiles), dim3(kTabTW, kTabTH), tab_smem, st>>>(
             f, row_begin, row_end, ctiles, pmin, pmax, psad);
         break;
       }
