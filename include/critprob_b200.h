@@ -226,6 +226,19 @@ int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t wi
                  int64_t n_samples, uint32_t channels, double* h_pmin, double* h_pmax,
                  double* h_psaddle, uint8_t* h_valid);
 
+/*
+ * Several models over ONE upload of the ensemble (the reference workflow
+ * `stack = EnsembleStack(v); for model: classify_field(from_ensemble(stack,
+ * model))`): every row chunk crossing PCIe is fitted for all n_models models
+ * while resident; then each model is classified and its planes copied back
+ * while the next model's stencil runs.  Model i is (kinds[i], bins[i], ks[i]);
+ * h_out[3*i + c] receives channel c (min, max, saddle) of model i (NULL skips).
+ */
+int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int64_t width,
+                        int32_t n_models, const int32_t* kinds, const int32_t* bins,
+                        const double* ks, int32_t method, uint64_t seed, int64_t n_samples,
+                        uint32_t channels, double* const* h_out, uint8_t* h_valid);
+
 /* Pinned host memory for cpb_run_host buffers. */
 int cpb_host_alloc(void** ptr, size_t bytes);
 int cpb_host_free(void* ptr);

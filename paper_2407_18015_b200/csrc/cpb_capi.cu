@@ -266,52 +266,86 @@ struct Streams {
 
 }  // namespace
 
-int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t width,
-                 int32_t kind, int32_t bins, double k, int32_t method, uint64_t seed,
-                 int64_t n_samples, uint32_t channels, double* h_pmin, double* h_pmax,
-                 double* h_psaddle, uint8_t* h_valid) {
+int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int64_t width,
+                        int32_t n_models, const int32_t* kinds, const int32_t* bins,
+                        const double* ks, int32_t method, uint64_t seed, int64_t n_samples,
+                        uint32_t channels, double* const* h_out, uint8_t* h_valid) {
   if (!h_ens || members < 1 || height < 1 || width < 1) {
     set_error("ensemble needs at least one member and one pixel");
     return CPB_EINVAL;
   }
   if (height < 3 || width < 3) { set_error("field must be at least 3 x 3 to have interior pixels"); return CPB_EINVAL; }
   if (method != 0 && method != 1) { set_error("method must be 0 (closed form) or 1 (monte carlo)"); return CPB_EINVAL; }
-  if (method == 0 && kind == CPB_GAUSSIAN) { set_error("Gaussian fields have no closed form; use monte_carlo"); return CPB_EINVAL; }
-  size_t pb[7];
-  int s = cpb_field_plane_bytes(kind, bins, (int32_t)members, height, width, pb);
-  if (s) return s;
-  Streams ss;
-  for (int i = 0; i < 2; ++i) {
-    cudaError_t e = cudaStreamCreateWithFlags(&ss.s[i], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_status(e, "stream setup");
+  if (n_models < 1 || n_models > 16 || !kinds || !bins || !ks) { set_error("1..16 models expected"); return CPB_EINVAL; }
+  for (int i = 0; i < n_models; ++i) {
+    if (method == 0 && kinds[i] == CPB_GAUSSIAN) { set_error("Gaussian fields have no closed form; use monte_carlo"); return CPB_EINVAL; }
+    if (members < 2 && (kinds[i] == CPB_EPANECHNIKOV || kinds[i] == CPB_GAUSSIAN)) {
+      set_error("%s fit needs at least two members", kinds[i] == CPB_EPANECHNIKOV ? "epanechnikov" : "gaussian");
+      return CPB_EINVAL;
+    }
   }
+  const int nm = n_models;
+  size_t pb[16][7];
+  int s;
+  for (int i = 0; i < nm; ++i)
+    if ((s = cpb_field_plane_bytes(kinds[i], bins[i], (int32_t)members, height, width, pb[i]))) return s;
+  Streams ss;  // s[0], s[1]: chunk ring (H2D + fits); s[0] then also classifies
+  cudaStream_t scopy = nullptr;
+  cudaError_t e = cudaStreamCreateWithFlags(&scopy, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&ss.s[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) return cuda_status(e, "stream setup");
+  struct CopyStream {
+    cudaStream_t s;
+    ~CopyStream() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
+  } copy_guard{scopy};
   cudaStream_t s0 = ss.s[0];
   const size_t plane = (size_t)height * width;
-  DevBuf lo, hi, mean, spread, wts, wtab, range, out;
-  if ((s = lo.alloc(pb[0], s0)) || (s = hi.alloc(pb[1], s0)) || (s = mean.alloc(pb[2], s0)) ||
-      (s = spread.alloc(pb[3], s0)) || (s = wts.alloc(pb[4], s0)) || (s = wtab.alloc(pb[5], s0)) ||
-      (s = range.alloc(pb[6], s0)) || (s = out.alloc(3 * plane * sizeof(double), s0)))
-    return s;
-  // row chunks of the ensemble, double-buffered: H2D of chunk i+1 overlaps the fit of chunk i
+  // per-model compact planes
+  DevBuf planes[16][7];
+  cpb_field fm[16];
+  for (int i = 0; i < nm; ++i) {
+    for (int q = 0; q < 7; ++q)
+      if ((s = planes[i][q].alloc(pb[i][q], s0))) return s;
+    cpb_field& f = fm[i];
+    f = cpb_field{};
+    f.kind = kinds[i]; f.bins = bins[i]; f.members = (int32_t)members;
+    f.height = height; f.width = width; f.row0 = 0; f.global_width = width;
+    f.k = ks[i]; f.eps = 0.0;
+    f.lo = planes[i][0].p; f.hi = planes[i][1].p; f.mean = (double*)planes[i][2].p;
+    f.spread = (double*)planes[i][3].p; f.weights = planes[i][4].p;
+    f.weight_table = (double*)planes[i][5].p;
+  }
+  // ping-pong output planes so the D2H of one model overlaps the next stencil
+  DevBuf out[2];
+  cudaEvent_t copied[2] = {nullptr, nullptr}, computed[2] = {nullptr, nullptr};
+  struct Events {  // destroyed before `out`: drains the copy stream before the buffers go
+    cudaEvent_t* a; cudaEvent_t* b; cudaStream_t cs;
+    ~Events() {
+      if (cs) cudaStreamSynchronize(cs);
+      for (int i = 0; i < 2; ++i) { if (a[i]) cudaEventDestroy(a[i]); if (b[i]) cudaEventDestroy(b[i]); }
+    }
+  } ev_guard{copied, computed, scopy};
+  for (int i = 0; i < 2; ++i) {
+    if ((s = out[i].alloc(3 * plane * sizeof(double), s0))) return s;
+    e = cudaMemsetAsync(out[i].p, 0, 3 * plane * sizeof(double), s0);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&computed[i], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e, "output setup");
+  }
+  // row chunks of the ensemble, double-buffered: the H2D of chunk j+1 overlaps the
+  // fits of chunk j; each chunk is fitted for every model while it is resident
   const size_t row_bytes = (size_t)members * width * sizeof(float);
   int64_t chunk = (int64_t)std::max<size_t>(1, (size_t)(256u << 20) / row_bytes);
   if (chunk > height) chunk = height;
   DevBuf ebuf[2];
   for (int i = 0; i < 2; ++i)
     if ((s = ebuf[i].alloc((size_t)chunk * row_bytes, s0))) return s;
-  cudaError_t e = cudaMemsetAsync(out.p, 0, 3 * plane * sizeof(double), s0);
-  if (e != cudaSuccess) return cuda_status(e, "memset");
   e = cudaEventRecord(ss.ev[0], s0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s[1], ss.ev[0], 0);
   if (e != cudaSuccess) return cuda_status(e, "event");
-
-  cpb_field f = {};
-  f.kind = kind; f.bins = bins; f.members = (int32_t)members;
-  f.height = height; f.width = width; f.row0 = 0; f.global_width = width;
-  f.k = k; f.eps = 0.0;
-  f.lo = lo.p; f.hi = hi.p; f.mean = (double*)mean.p; f.spread = (double*)spread.p;
-  f.weights = wts.p; f.weight_table = (double*)wtab.p;
   int nchunks = 0;
   for (int64_t r0 = 0; r0 < height; r0 += chunk, ++nchunks) {
     const int64_t nr = std::min(chunk, height - r0);
@@ -322,51 +356,66 @@ int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t wi
                           plane * sizeof(float), (size_t)nr * width * sizeof(float), (size_t)members,
                           cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_status(e, "H2D ensemble chunk");
-    cpb_field fc = f;
-    const size_t off = (size_t)r0 * width;
-    fc.height = nr;
-    fc.lo = (char*)lo.p + off * (pb[0] ? sizeof(float) : 0);
-    fc.hi = (char*)hi.p + off * (pb[1] ? sizeof(float) : 0);
-    fc.mean = pb[2] ? (double*)mean.p + off : nullptr;
-    fc.spread = pb[3] ? (double*)spread.p + off : nullptr;
-    // bin planes are (bins, H, W): the chunk view offsets the base pointer and
-    // keeps the full-grid plane stride
-    fc.weights = pb[4] ? (char*)wts.p + off * (members <= 255 ? 1 : 2) : nullptr;
-    fc.plane_stride = (int64_t)plane;
     // range accumulation is serialised across the two streams by the chunk order
     if (nchunks > 0) {
       e = cudaStreamWaitEvent(st, ss.ev[b ^ 1], 0);
       if (e != cudaSuccess) return cuda_status(e, "event wait");
     }
-    if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc, (uint32_t*)range.p,
-                     nchunks > 0, st)))
-      return s;
-    f.bounds = fc.bounds;
-    f.weights_mode = fc.weights_mode;
+    const size_t off = (size_t)r0 * width;
+    for (int i = 0; i < nm; ++i) {
+      cpb_field fc = fm[i];
+      fc.height = nr;
+      fc.lo = pb[i][0] ? (char*)planes[i][0].p + off * sizeof(float) : nullptr;
+      fc.hi = pb[i][1] ? (char*)planes[i][1].p + off * sizeof(float) : nullptr;
+      fc.mean = pb[i][2] ? (double*)planes[i][2].p + off : nullptr;
+      fc.spread = pb[i][3] ? (double*)planes[i][3].p + off : nullptr;
+      // bin planes are (bins, H, W): the chunk view offsets the base pointer and
+      // keeps the full-grid plane stride
+      fc.weights = pb[i][4] ? (char*)planes[i][4].p + off * (members <= 255 ? 1 : 2) : nullptr;
+      fc.plane_stride = (int64_t)plane;
+      if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc,
+                       (uint32_t*)planes[i][6].p, nchunks > 0, st)))
+        return s;
+      fm[i].bounds = fc.bounds;
+      fm[i].weights_mode = fc.weights_mode;
+    }
     e = cudaEventRecord(ss.ev[b], st);
     if (e != cudaSuccess) return cuda_status(e, "event record");
   }
   e = cudaStreamWaitEvent(s0, ss.ev[(nchunks - 1) & 1], 0);
   if (e != cudaSuccess) return cuda_status(e, "event wait");
-  double gmin = 0.0, gmax = 0.0;
-  if ((s = cpb_read_range((const uint32_t*)range.p, &gmin, &gmax, s0))) return s;
-  f.eps = cpb_epsilon(gmin, gmax);
-  double* pmin = (double*)out.p;
-  double* pmax = pmin + plane;
-  double* psad = pmax + plane;
-  double* om = (channels & CPB_CH_MIN) ? pmin : nullptr;
-  double* oM = (channels & CPB_CH_MAX) ? pmax : nullptr;
-  double* oS = (channels & CPB_CH_SADDLE) ? psad : nullptr;
-  if (method == 0)
-    s = cpb_classify_closed(&f, 1, height - 1, om, oM, oS, s0);
-  else
-    s = cpb_classify_mc(&f, 1, height - 1, seed, n_samples, CPB_RNG_SPLITMIX, om, oM, oS, nullptr, s0);
-  if (s) return s;
-  double* dst[3] = {h_pmin, h_pmax, h_psaddle};
-  for (int c = 0; c < 3; ++c) {
-    if (!dst[c]) continue;
-    e = cudaMemcpyAsync(dst[c], pmin + c * plane, plane * sizeof(double), cudaMemcpyDeviceToHost, s0);
-    if (e != cudaSuccess) return cuda_status(e, "D2H probabilities");
+  for (int i = 0; i < nm; ++i) {
+    double gmin = 0.0, gmax = 0.0;
+    if ((s = cpb_read_range((const uint32_t*)planes[i][6].p, &gmin, &gmax, s0))) return s;
+    fm[i].eps = cpb_epsilon(gmin, gmax);
+    const int o = i & 1;
+    if (i >= 2) {  // the D2H of model i-2 must be done with this buffer
+      e = cudaStreamWaitEvent(s0, copied[o], 0);
+      if (e != cudaSuccess) return cuda_status(e, "event wait");
+    }
+    double* pmin = (double*)out[o].p;
+    double* pmax = pmin + plane;
+    double* psad = pmax + plane;
+    double* om = (channels & CPB_CH_MIN) ? pmin : nullptr;
+    double* oM = (channels & CPB_CH_MAX) ? pmax : nullptr;
+    double* oS = (channels & CPB_CH_SADDLE) ? psad : nullptr;
+    if (method == 0)
+      s = cpb_classify_closed(&fm[i], 1, height - 1, om, oM, oS, s0);
+    else
+      s = cpb_classify_mc(&fm[i], 1, height - 1, seed, n_samples, CPB_RNG_SPLITMIX, om, oM, oS,
+                          nullptr, s0);
+    if (s) return s;
+    e = cudaEventRecord(computed[o], s0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(scopy, computed[o], 0);
+    if (e != cudaSuccess) return cuda_status(e, "event");
+    for (int c = 0; c < 3; ++c) {
+      double* dst = h_out ? h_out[3 * i + c] : nullptr;
+      if (!dst) continue;
+      e = cudaMemcpyAsync(dst, pmin + c * plane, plane * sizeof(double), cudaMemcpyDeviceToHost, scopy);
+      if (e != cudaSuccess) return cuda_status(e, "D2H probabilities");
+    }
+    e = cudaEventRecord(copied[o], scopy);
+    if (e != cudaSuccess) return cuda_status(e, "event record");
   }
   if (h_valid) {
     for (int64_t r = 0; r < height; ++r) {
@@ -377,9 +426,19 @@ int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t wi
       row[width - 1] = 0;
     }
   }
-  e = cudaStreamSynchronize(s0);
+  e = cudaStreamSynchronize(scopy);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s0);
   if (e != cudaSuccess) return cuda_status(e, "synchronize");
   return CPB_OK;
+}
+
+int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t width,
+                 int32_t kind, int32_t bins, double k, int32_t method, uint64_t seed,
+                 int64_t n_samples, uint32_t channels, double* h_pmin, double* h_pmax,
+                 double* h_psaddle, uint8_t* h_valid) {
+  double* outs[3] = {h_pmin, h_pmax, h_psaddle};
+  return cpb_run_host_models(h_ens, members, height, width, 1, &kind, &bins, &k, method, seed,
+                             n_samples, channels, outs, h_valid);
 }
 
 }  // extern "C"
