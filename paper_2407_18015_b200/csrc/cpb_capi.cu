@@ -4,6 +4,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -338,7 +339,12 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
   // row chunks of the ensemble, double-buffered: the H2D of chunk j+1 overlaps the
   // fits of chunk j; each chunk is fitted for every model while it is resident
   const size_t row_bytes = (size_t)members * width * sizeof(float);
-  int64_t chunk = (int64_t)std::max<size_t>(1, (size_t)(256u << 20) / row_bytes);
+  // chunk bytes (CPB_HOST_CHUNK_BYTES overrides, for tests of the chunked path)
+  static const size_t chunk_bytes = [] {
+    const char* e = getenv("CPB_HOST_CHUNK_BYTES");
+    return e ? (size_t)atoll(e) : (size_t)(256u << 20);
+  }();
+  int64_t chunk = (int64_t)std::max<size_t>(1, chunk_bytes / row_bytes);
   if (chunk > height) chunk = height;
   DevBuf ebuf[2];
   for (int i = 0; i < 2; ++i)

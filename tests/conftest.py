@@ -20,3 +20,7 @@ def golden():
 
     return {name: dict(np.load(os.path.join(GOLDEN, name + ".npz")))
             for name in ("fit", "closed", "mc", "rng", "semi")}
+
+# small host-path chunks so the GPU tests exercise cpb_run_host's chunked
+# upload and chunk views (the library reads this once, at first use)
+os.environ.setdefault("CPB_HOST_CHUNK_BYTES", str(64 * 1024))

@@ -348,3 +348,43 @@ def test_semianalytical_close_to_closed_form():
         assert np.max(np.abs(semi.channel(ch) - ref[ch])) <= SEMI_TOL
     with pytest.raises(ValueError):
         cpb.classify_field(_fit(vals, "uniform"), cpb.EstimatorSpec(method="semianalytical"))
+
+
+# ---------------------------------------------------------------- one-call host path
+def test_run_host_models_matches_oracle():
+    """cpb_run_host_models / cpb_run_host: host buffers in, host planes out (C ABI)."""
+    import ctypes
+
+    from paper_2407_18015_b200 import _lib
+
+    lib = _lib.load()
+    # conftest sets CPB_HOST_CHUNK_BYTES small: the row-chunked H2D + chunk views path
+    vals = np.ascontiguousarray(orc.ackley_ensemble(37, 4099, 6, noise_amp=0.3, seed=3))
+    M, H, W = vals.shape
+    models = [("uniform", 5), ("epanechnikov", 5), ("histogram", 4)]
+    outs = [np.zeros((H, W)) for _ in range(3 * len(models))]
+    valid = np.zeros((H, W), dtype=np.uint8)
+    kinds = (ctypes.c_int32 * 3)(*[_lib.KIND_CODES[k] for k, _ in models])
+    bins = (ctypes.c_int32 * 3)(*[b for _, b in models])
+    ks = (ctypes.c_double * 3)(*[float(cpb.ModelSpec(k).k) for k, _ in models])
+    ptrs = (ctypes.c_void_p * 9)(*[o.ctypes.data for o in outs])
+    _lib.check(lib.cpb_run_host_models(vals.ctypes.data, M, H, W, 3, kinds, bins, ks, 0, 0, 0, 7,
+                                       ptrs, valid.ctypes.data))
+    assert valid[1:-1, 1:-1].all() and not valid[0].any() and not valid[:, -1].any()
+    for i, (kind, b) in enumerate(models):
+        ref = orc.classify(orc.fit(vals, kind, b), kind)
+        for c, ch in enumerate(("min", "max", "saddle")):
+            assert np.max(np.abs(outs[3 * i + c] - ref[ch])) <= CLOSED_TOL, (kind, ch)
+    # single-model entry point, Monte Carlo
+    o = [np.zeros((H, W)) for _ in range(3)]
+    _lib.check(lib.cpb_run_host(vals.ctypes.data, M, H, W, 0, 5, 1.0, 1, 11, 300, 7,
+                                o[0].ctypes.data, o[1].ctypes.data, o[2].ctypes.data, None))
+    ref = orc.classify(orc.fit(vals, "uniform"), "uniform", method="monte_carlo", n_samples=300,
+                       seed=11)
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(o[c], ref[ch])
+    bad = vals.copy()
+    bad[2, 7, 7] = np.nan
+    with pytest.raises(ValueError):
+        _lib.check(lib.cpb_run_host(bad.ctypes.data, M, H, W, 0, 5, 1.0, 0, 0, 0, 7,
+                                    o[0].ctypes.data, None, None, None))
