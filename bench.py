@@ -71,6 +71,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--serial", action="store_true", help="no fit/stencil overlap (one stream)")
+    p.add_argument("--fit-ctas", type=int, default=0,
+                   help="persistent fit CTAs per SM while overlapping (0 = occupancy maximum)")
     p.add_argument("--profile", action="store_true", help="one short pass, for ncu")
     return p.parse_args()
 
@@ -193,6 +195,10 @@ def run_ours(args):
     fitted = {k: torch.cuda.Event() for k in models}
     consumed = {k: torch.cuda.Event() for k in models}
     overlap = not args.serial
+    if overlap and args.fit_ctas:
+        from paper_2407_18015_b200 import _lib
+
+        _lib.check(_lib.load().cpb_set_option(b"fit_ctas_per_sm", args.fit_ctas))
 
     def step():
         for kind in models:

@@ -117,6 +117,12 @@ typedef struct cpb_field {
 int cpb_abi_version(void);
 const char* cpb_last_error(void);
 
+/* Process-wide tunables (results never depend on them):
+ *   "fit_ctas_per_sm"  cap on the persistent fit CTAs per SM (0 = occupancy
+ *                      maximum); a smaller fit footprint lets a stencil running
+ *                      on another stream share the SMs. */
+int cpb_set_option(const char* name, int64_t value);
+
 /* Bytes of device memory each plane of a fitted field needs
  * (lo, hi, mean, spread, weights, weight_table, range scratch), written into
  * out[7].  Mirrors the layout cpb_fit writes. */

@@ -41,6 +41,7 @@ class CpbField(ctypes.Structure):
 _SIGNATURES = {
     "cpb_abi_version": (c_i32, []),
     "cpb_last_error": (ctypes.c_char_p, []),
+    "cpb_set_option": (c_i32, [ctypes.c_char_p, c_i64]),
     "cpb_epsilon": (c_dbl, [c_dbl, c_dbl]),
     "cpb_field_plane_bytes": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
     "cpb_fit": (c_i32, [c_vp, c_i64, ctypes.POINTER(CpbField), c_vp, c_i32, c_vp]),

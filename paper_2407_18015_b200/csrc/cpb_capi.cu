@@ -31,6 +31,8 @@ int launch_unit_block(uint64_t seed, const uint64_t* px, int64_t npix, int plane
 int launch_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t c,
                 double* pmin, double* pmax, double* psad, cudaStream_t st);
 
+extern int g_fit_ctas_per_sm;
+
 static thread_local char g_err[512] = "";
 
 void set_error(const char* fmt, ...) {
@@ -64,6 +66,17 @@ using namespace cpb;
 extern "C" {
 
 int cpb_abi_version(void) { return CPB_ABI_VERSION; }
+
+int cpb_set_option(const char* name, int64_t value) {
+  if (!name) { set_error("NULL option name"); return CPB_EINVAL; }
+  if (strcmp(name, "fit_ctas_per_sm") == 0) {
+    if (value < 0 || value > 32) { set_error("fit_ctas_per_sm must be in [0, 32]"); return CPB_EINVAL; }
+    g_fit_ctas_per_sm = (int)value;
+    return CPB_OK;
+  }
+  set_error("unknown option %s", name);
+  return CPB_EINVAL;
+}
 
 const char* cpb_last_error(void) { return g_err; }
 

@@ -584,6 +584,10 @@ inline unsigned grid_for(int64_t n, int threads) { return (unsigned)((n + thread
 
 }  // namespace
 
+// cap on persistent fit CTAs per SM (0 = occupancy maximum); a smaller fit
+// footprint leaves room for a concurrent stencil (cpb_set_option "fit_ctas_per_sm")
+int g_fit_ctas_per_sm = 0;
+
 int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range, bool accumulate,
                cudaStream_t st) {
   FitArgs a;
@@ -651,6 +655,7 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);          \
     int per_sm = 1;                                                                              \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaTile, smem);                \
+    if (g_fit_ctas_per_sm > 0) per_sm = std::min(per_sm, g_fit_ctas_per_sm);                    \
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
     kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);            \
   } while (0)
