@@ -444,7 +444,7 @@ constexpr int kPPFields = 18;  // m[5], ih[5], lo[1..4], hi[1..4]
 struct PPWarpSmem {
   double vd[kPPFields][32];  // vertex constants, SoA
   double pa[9 * 32], pb[9 * 32];
-  double res[9 * 32][4];
+  double res[9 * 32][3];  // per piece: min, max, saddle (t1 + t2)
   unsigned char owner[9 * 32];
   unsigned char fast[32];
 };
@@ -647,7 +647,9 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_ada_kernel(
       const double half = 0.5 * (b - a);
       const int sl = S.slot[e];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) S.res[sl][r] = mk[r] ? s[r] * half : 0.0;
+      S.res[sl][0] = mk[0] ? s[0] * half : 0.0;
+      S.res[sl][1] = mk[1] ? s[1] * half : 0.0;
+      S.res[sl][2] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
     }
     cbase += ctot[q];
   }
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_ada_kernel(
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int q = off; q < off + n; ++q) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] += S.res[q][r];
+      for (int r = 0; r < 3; ++r) acc[r] += S.res[q][r];
     }
     store(pmin, pmax, psad, idx, acc);
   }
@@ -783,14 +785,16 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     }
     const double half = 0.5 * (b - a);
 #pragma unroll
-    for (int r = 0; r < 4; ++r) S.res[e][r] = mk[r] ? s[r] * half : 0.0;
+    S.res[e][0] = mk[0] ? s[0] * half : 0.0;
+    S.res[e][1] = mk[1] ? s[1] * half : 0.0;
+    S.res[e][2] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
   }
   __syncwarp();
   if (live) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int q = off; q < off + n; ++q) {
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] += S.res[q][r];
+      for (int r = 0; r < 3; ++r) acc[r] += S.res[q][r];
     }
     if (KIND == CPB_UNIFORM) {
       const double pdf = S.vd[10][lane];  // 1 / (hi_C - lo_C)
