@@ -199,6 +199,16 @@ int cpb_classify_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, ui
                       void* stream);
 
 /*
+ * Combinatorial (Eq. 5) cross-check, histogram fields with bins <= 8
+ * (engine.py:320-404, grid chunk engine.py:686-702): sum over all bins^5
+ * bin combinations of the bin-mass product times the all-uniform
+ * probabilities.  Agrees with the closed form to ~1e-12 (the reference's own
+ * acceptance bar is 1e-9, test_acceptance.py:100-108).
+ */
+int cpb_classify_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end,
+                               double* d_pmin, double* d_pmax, double* d_psaddle, void* stream);
+
+/*
  * Reference-layout float64 parameters (fields.py:86-103, what from_ensemble
  * returns): uniform/histogram -> d_a = lo, d_b = hi (widened),
  * d_weights = (H, W, bins) weights; epanechnikov -> d_a = mean,

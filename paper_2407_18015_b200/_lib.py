@@ -54,6 +54,8 @@ _SIGNATURES = {
                                 c_vp, c_vp, c_vp, c_vp, c_vp]),
     "cpb_classify_semi": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_u64, c_i64, c_vp, c_vp,
                                   c_vp, c_vp]),
+    "cpb_classify_combinatorial": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_vp, c_vp, c_vp,
+                                           c_vp]),
     "cpb_materialize": (c_i32, [ctypes.POINTER(CpbField), c_vp, c_vp, c_vp, c_vp]),
     "cpb_unit_block": (c_i32, [c_u64, c_vp, c_i64, c_i32, c_i64, c_i64, c_vp, c_vp]),
     "cpb_synth_ensemble": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i64, c_i64, c_dbl, c_u64, c_vp]),

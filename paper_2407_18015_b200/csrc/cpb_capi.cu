@@ -30,6 +30,8 @@ int launch_unit_block(uint64_t seed, const uint64_t* px, int64_t npix, int plane
                       int64_t n, double* out, cudaStream_t st);
 int launch_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t c,
                 double* pmin, double* pmax, double* psad, cudaStream_t st);
+int launch_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end, double* pmin,
+                         double* pmax, double* psad, cudaStream_t st);
 
 extern int g_fit_ctas_per_sm;
 
@@ -210,6 +212,21 @@ int cpb_classify_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, ui
   }
   return launch_semi(f, row_begin, row_end, seed, c, d_pmin, d_pmax, d_psaddle,
                      (cudaStream_t)stream);
+}
+
+int cpb_classify_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end,
+                               double* d_pmin, double* d_pmax, double* d_psaddle, void* stream) {
+  int s = check_field(f, true);
+  if (s) return s;
+  if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
+    if (row_end > row_begin) {
+      set_error("rows [%lld, %lld) need a one-row halo inside the field",
+                (long long)row_begin, (long long)row_end);
+      return CPB_EINVAL;
+    }
+  }
+  return launch_combinatorial(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle,
+                              (cudaStream_t)stream);
 }
 
 int cpb_materialize(const cpb_field* f, double* d_a, double* d_b, double* d_weights,

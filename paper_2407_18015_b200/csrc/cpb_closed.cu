@@ -251,16 +251,13 @@ CPB_D void uniform_piece(double a, double b, const double* lo, const double* hi,
   range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
 }
 
-__global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
-    FieldView f, Window w, double* pmin, double* pmax, double* psad) {
-  int64_t idx;
-  if (!vertex(f, w, idx)) return;
-  const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
-  double lo[5], hi[5], inv[5];
+// The four integrals (min, max, saddle t1, t2) of one all-uniform
+// neighbourhood given its five supports [lo_P, hi_P] (P = C, E, N, W, S).
+CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) {
+  double inv[5];
   bool fast = true;
 #pragma unroll
   for (int p = 0; p < 5; ++p) {
-    load_bounds(f, at[p], lo[p], hi[p]);
     inv[p] = 1.0 / (hi[p] - lo[p]);
     fast &= (fabs(lo[p]) + fabs(hi[p])) * inv[p] <= kFastRatio;
   }
@@ -271,12 +268,120 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
     k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
   }
   merge_pairs8(k);
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int r = 0; r < 4; ++r) acc[r] = 0.0;
   if (fast) uniform_pieces<true>(lo, hi, inv, k, acc);
   else uniform_pieces<false>(lo, hi, inv, k, acc);
 #pragma unroll
   for (int r = 0; r < 4; ++r) acc[r] *= inv[C_];
+}
+
+__global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
+    FieldView f, Window w, double* pmin, double* pmax, double* psad) {
+  int64_t idx;
+  if (!vertex(f, w, idx)) return;
+  const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+  double lo[5], hi[5];
+#pragma unroll
+  for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+  double acc[4];
+  uniform_integrals(lo, hi, acc);
   store(pmin, pmax, psad, idx, acc);
+}
+
+// --------------------------------------------------------- combinatorial
+// Eq. 5 cross-check for histogram fields (engine.py:320-404, grid chunk
+// engine.py:686-702): the sum over every combination of one bin per position
+// of (product of the bin masses) x (the all-uniform probability with each
+// position uniform on its bin).  One warp per vertex; lanes take combinations
+// (C index slowest, itertools.product order) and the all-uniform terms come
+// from uniform_integrals; a fixed warp tree adds the lane partials.
+// Weights are renormalised like dist.histogram (w / w.sum(), a 1-D numpy
+// pairwise sum) and the bin edges are lo + (hi - lo) * k / h
+// (_histogram_grid, engine.py:313-317).
+constexpr int kCombWarps = 4;
+constexpr int COMB_MAX_BINS = 8;  // COMBINATORIAL_MAX_BINS, engine.py:44
+
+__global__ void __launch_bounds__(kCombWarps * 32) combinatorial_kernel(
+    FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
+    double* psad) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t v = (int64_t)blockIdx.x * kCombWarps + warp;
+  if (v >= nvert) return;
+  const int h = f.bins;
+  const int64_t r = row_begin + v / cols, c = 1 + v % cols;
+  const int64_t idx = r * f.width + c;
+  const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+  double wn[5][COMB_MAX_BINS], edge[5][COMB_MAX_BINS + 1];
+#pragma unroll
+  for (int p = 0; p < 5; ++p) {
+    double lo, hi;
+    const bool deg = load_bounds(f, at[p], lo, hi);
+    const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at[p]), lo, hi, h) : 0;
+    double w[COMB_MAX_BINS];
+#pragma unroll
+    for (int b = 0; b < COMB_MAX_BINS; ++b) w[b] = b < h ? load_weight(f, at[p], b, deg, dbin) : 0.0;
+    double total = 0.0;  // numpy pairwise sum, h <= 8: sequential below 8 terms
+    if (h < 8) {
+#pragma unroll
+      for (int b = 0; b < COMB_MAX_BINS; ++b)
+        if (b < h) total = __dadd_rn(total, w[b]);
+    } else {
+      total = __dadd_rn(__dadd_rn(__dadd_rn(w[0], w[1]), __dadd_rn(w[2], w[3])),
+                        __dadd_rn(__dadd_rn(w[4], w[5]), __dadd_rn(w[6], w[7])));
+    }
+#pragma unroll
+    for (int b = 0; b < COMB_MAX_BINS; ++b) wn[p][b] = b < h ? __ddiv_rn(w[b], total) : 0.0;
+    const double width = __dsub_rn(hi, lo);
+#pragma unroll
+    for (int b = 0; b <= COMB_MAX_BINS; ++b)
+      edge[p][b] = b <= h ? __dadd_rn(lo, __ddiv_rn(__dmul_rn(width, (double)b), (double)h)) : 0.0;
+  }
+  int64_t ncomb = 1;
+  for (int p = 0; p < 5; ++p) ncomb *= h;
+  double s_min = 0.0, s_max = 0.0, s_sad = 0.0;
+  for (int64_t q = lane; q < ncomb; q += 32) {
+    int64_t rest = q;
+    int ib[5];
+#pragma unroll
+    for (int p = 4; p >= 0; --p) {
+      ib[p] = (int)(rest % h);
+      rest /= h;
+    }
+    double wprod = 1.0, lo[5], hi[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      double wb = 0.0, a = 0.0, b = 0.0;
+#pragma unroll
+      for (int k = 0; k < COMB_MAX_BINS; ++k) {
+        if (k == ib[p]) {
+          wb = wn[p][k];
+          a = edge[p][k];
+          b = edge[p][k + 1];
+        }
+      }
+      wprod = __dmul_rn(wprod, wb);
+      lo[p] = a;
+      hi[p] = b;
+    }
+    if (wprod == 0.0) continue;
+    double t[4];
+    uniform_integrals(lo, hi, t);
+    s_min = fma(wprod, t[0], s_min);
+    s_max = fma(wprod, t[1], s_max);
+    s_sad = fma(wprod, t[2] + t[3], s_sad);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    s_min += __shfl_xor_sync(0xffffffffu, s_min, d);
+    s_max += __shfl_xor_sync(0xffffffffu, s_max, d);
+    s_sad += __shfl_xor_sync(0xffffffffu, s_sad, d);
+  }
+  if (lane == 0) {
+    if (pmin) pmin[idx] = s_min;
+    if (pmax) pmax[idx] = s_max;
+    if (psad) psad[idx] = s_sad;
+  }
 }
 
 // ------------------------------------------------------------ epanechnikov
@@ -1313,6 +1418,26 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
 }
 
 }  // namespace
+
+int launch_combinatorial(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
+                         double* pmax, double* psad, cudaStream_t st) {
+  const FieldView f = make_view(*fld);
+  if (f.kind != CPB_HISTOGRAM) {
+    set_error("combinatorial estimation is defined for histogram fields only");
+    return CPB_EINVAL;
+  }
+  if (f.bins > COMB_MAX_BINS) {
+    set_error("combinatorial estimation refuses more than %d bins", COMB_MAX_BINS);
+    return CPB_EINVAL;
+  }
+  const int64_t rows = row_end - row_begin;
+  if (rows <= 0 || f.width < 3) return CPB_OK;
+  const int64_t cols = f.width - 2, nvert = rows * cols;
+  combinatorial_kernel<<<(unsigned)((nvert + kCombWarps - 1) / kCombWarps), kCombWarps * 32, 0, st>>>(
+      f, row_begin, nvert, cols, pmin, pmax, psad);
+  CPB_CHECK_LAUNCH("combinatorial kernel");
+  return CPB_OK;
+}
 
 int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
                   double* pmax, double* psad, cudaStream_t st) {

@@ -9,11 +9,9 @@ Mirrors the grid entry points of critprob.engine
                       as in the reference, never changes the result)
 - ``pixel_index``     engine.py:482-484
 
-Closed form runs ``cpb_classify_closed``, Monte Carlo ``cpb_classify_mc``
-and the semianalytical estimator ``cpb_classify_semi``
-(include/critprob_b200.h).  The combinatorial estimator (a cross-check
-oracle in the reference, engine.py:320-404) is not on the B200 path yet and
-raises NotImplementedError.
+Closed form runs ``cpb_classify_closed``, Monte Carlo ``cpb_classify_mc``,
+the semianalytical estimator ``cpb_classify_semi`` and the combinatorial
+(Eq. 5) cross-check ``cpb_classify_combinatorial`` (include/critprob_b200.h).
 """
 
 from __future__ import annotations
@@ -103,9 +101,9 @@ def run_rows(dev, estimator: EstimatorSpec, channels, row_begin: int, row_end: i
         seed = int(estimator.seed) & ((1 << 64) - 1)
         _lib.check(lib.cpb_classify_semi(dev.ref(), row_begin, row_end, seed, int(estimator.c),
                                          _lib.ptr(pm), _lib.ptr(pM), _lib.ptr(pS), s))
-    else:
-        raise NotImplementedError(
-            f"the {estimator.method} estimator is not on the B200 path yet")
+    else:  # combinatorial (validated: histogram, bins <= COMBINATORIAL_MAX_BINS)
+        _lib.check(lib.cpb_classify_combinatorial(dev.ref(), row_begin, row_end, _lib.ptr(pm),
+                                                  _lib.ptr(pM), _lib.ptr(pS), s))
 
 
 def classify_field(
@@ -128,8 +126,6 @@ def classify_field(
 
     estimator = estimator or EstimatorSpec()
     channels = _validate(field, estimator, workers, channels)
-    if estimator.method == "combinatorial":
-        raise NotImplementedError("the combinatorial estimator is not on the B200 path yet")
     dev = field.device_field()
     H, W = field.shape
     planes = torch.zeros((3, H, W), dtype=torch.float64, device=dev.device)

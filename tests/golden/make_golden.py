@@ -14,6 +14,7 @@ The fixtures travel with the repo; nothing at test time reads
 - classify_field closed form    (engine.py:716-787, 594-629)
 - classify_field Monte Carlo    (engine.py:659-666, 632-656)
 - classify_field semianalytical (engine.py:669-683)
+- classify_field combinatorial  (engine.py:686-702)
 - rngstream.unit_block          (rngstream.py:33-48)
 """
 
@@ -78,6 +79,7 @@ def main() -> None:
     closed = {}
     mc = {}
     semi = {}
+    comb = {}
     for name, vals in ens.items():
         fit[f"ens/{name}"] = vals
         stack = EnsembleStack(vals)
@@ -101,6 +103,12 @@ def main() -> None:
                 for ch in ("min", "max", "saddle"):
                     mc[f"{tag}/{ch}"] = prob.channel(ch)
                 mc[f"{tag}/n"] = np.array(n)
+            if kind == "histogram" and (bins in (1, 3) or (bins == 5 and name == "degenerate")) \
+                    and name in ("ackley", "rand", "degenerate", "offset"):
+                prob = classify_field(field, EstimatorSpec(method="combinatorial"))
+                for ch in ("min", "max", "saddle"):
+                    comb[f"{tag}/{ch}"] = prob.channel(ch)
+                comb[f"{tag}/done"] = np.array(1)
             if kind == "histogram" and name in ("ackley", "rand", "degenerate") and bins in (3, 5, 9):
                 est = EstimatorSpec(method="semianalytical", c=700, seed=2)
                 prob = classify_field(field, est)
@@ -145,7 +153,8 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "mc.npz"), **mc)
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **rng_fx)
     np.savez_compressed(os.path.join(HERE, "semi.npz"), **semi)
-    for f in ("fit", "closed", "mc", "rng", "semi"):
+    np.savez_compressed(os.path.join(HERE, "comb.npz"), **comb)
+    for f in ("fit", "closed", "mc", "rng", "semi", "comb"):
         print(f, os.path.getsize(os.path.join(HERE, f + ".npz")), "bytes")
 
 

@@ -388,3 +388,29 @@ def test_run_host_models_matches_oracle():
     with pytest.raises(ValueError):
         _lib.check(lib.cpb_run_host(bad.ctypes.data, M, H, W, 0, 5, 1.0, 0, 0, 0, 7,
                                     o[0].ctypes.data, None, None, None))
+
+
+# ---------------------------------------------------------------- combinatorial (Eq. 5)
+COMB_TOL = 1e-12  # the reference evaluates each all-uniform term exactly; we use 3-node GL
+
+
+def test_combinatorial_against_reference(golden):
+    fit, comb = golden["fit"], golden["comb"]
+    seen = 0
+    for key in comb:
+        parts = key.split("/")
+        if len(parts) != 4 or parts[3] != "done":
+            continue
+        name, kind, bins = parts[0], parts[1], int(parts[2])
+        field = _fit(fit[f"ens/{name}"], kind, bins)
+        prob = cpb.classify_field(field, cpb.EstimatorSpec(method="combinatorial"))
+        closed = cpb.classify_field(field)
+        for ch in ("min", "max", "saddle"):
+            ref = comb[f"{name}/{kind}/{bins}/{ch}"]
+            assert np.max(np.abs(prob.channel(ch) - ref)) <= COMB_TOL, (key, ch)
+            # test_acceptance.py:100-108: Eq. 5 agrees with the factorised form
+            assert np.max(np.abs(prob.channel(ch) - closed.channel(ch))) <= 1e-9, (key, ch)
+        seen += 1
+    assert seen >= 8
+    with pytest.raises(ValueError):
+        cpb.classify_field(_fit(fit["ens/rand"], "histogram", 9), cpb.EstimatorSpec(method="combinatorial"))
