@@ -255,6 +255,12 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
                         const double* ks, int32_t method, uint64_t seed, int64_t n_samples,
                         uint32_t channels, double* const* h_out, uint8_t* h_valid);
 
+/* P5 heatmap bytes of one probability plane (export_heatmap, field_io.py:138-150):
+ * d_out[i] = round_half_even(255 * clip(d_p[i], 0, 1)^gamma), 0 where d_valid[i]
+ * is 0 (d_valid may be NULL). */
+int cpb_heatmap(const double* d_p, const uint8_t* d_valid, int64_t n, double gamma,
+                uint8_t* d_out, void* stream);
+
 /* Pinned host memory for cpb_run_host buffers. */
 int cpb_host_alloc(void** ptr, size_t bytes);
 int cpb_host_free(void* ptr);

@@ -24,6 +24,20 @@ from .fields import (
     UncertainField,
     set_device,
 )
+from .field_io import (
+    UcvfError,
+    UcvfFormatError,
+    UcvfPayloadError,
+    UcvfValueError,
+    export_heatmap,
+    load_ensemble,
+    load_probability_field,
+    load_scalar_field,
+    save_ensemble,
+    save_probability_field,
+    save_scalar_field,
+    uniform_field_from_scalar,
+)
 from .rngstream import unit_block, unit_planes
 from .synth import synthetic_ensemble, synthetic_rows
 
@@ -31,5 +45,8 @@ __all__ = [
     "CHANNELS", "COMBINATORIAL_MAX_BINS", "ESTIMATOR_METHODS", "MODEL_KINDS", "PATTERNS",
     "EnsembleStack", "EstimatorSpec", "ModelSpec", "ProbabilityField", "UncertainField",
     "classify_field", "pixel_index", "set_device", "synthetic_ensemble", "synthetic_rows",
-    "unit_block", "unit_planes",
+    "unit_block", "unit_planes", "UcvfError", "UcvfFormatError", "UcvfPayloadError",
+    "UcvfValueError", "export_heatmap", "load_ensemble", "load_probability_field",
+    "load_scalar_field", "save_ensemble", "save_probability_field", "save_scalar_field",
+    "uniform_field_from_scalar",
 ]

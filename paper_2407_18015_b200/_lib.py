@@ -64,6 +64,7 @@ _SIGNATURES = {
     "cpb_run_host_models": (c_i32, [c_vp, c_i64, c_i64, c_i64, c_i32, ctypes.POINTER(c_i32),
                                     ctypes.POINTER(c_i32), ctypes.POINTER(c_dbl), c_i32, c_u64,
                                     c_i64, c_u32, ctypes.POINTER(c_vp), c_vp]),
+    "cpb_heatmap": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "cpb_host_alloc": (c_i32, [ctypes.POINTER(c_vp), ctypes.c_size_t]),
     "cpb_host_free": (c_i32, [c_vp]),
 }

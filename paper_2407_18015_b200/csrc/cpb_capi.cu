@@ -32,6 +32,8 @@ int launch_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t
                 double* pmin, double* pmax, double* psad, cudaStream_t st);
 int launch_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end, double* pmin,
                          double* pmax, double* psad, cudaStream_t st);
+int launch_heatmap(const double* p, const uint8_t* valid, int64_t n, double gamma, uint8_t* out,
+                   cudaStream_t st);
 
 extern int g_fit_ctas_per_sm;
 
@@ -250,6 +252,13 @@ int cpb_synth_ensemble(float* d_ens, int64_t members, int64_t row0, int64_t nrow
   }
   return launch_synth(d_ens, members, row0, nrows, width, height, noise_amp, seed,
                       (cudaStream_t)stream);
+}
+
+int cpb_heatmap(const double* d_p, const uint8_t* d_valid, int64_t n, double gamma,
+                uint8_t* d_out, void* stream) {
+  if (!(gamma > 0.0)) { set_error("gamma must be positive"); return CPB_EINVAL; }
+  if (n < 0 || (n > 0 && (!d_p || !d_out))) { set_error("invalid heatmap buffers"); return CPB_EINVAL; }
+  return launch_heatmap(d_p, d_valid, n, gamma, d_out, (cudaStream_t)stream);
 }
 
 int cpb_host_alloc(void** ptr, size_t bytes) {

@@ -788,3 +788,33 @@ int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64
 }
 
 }  // namespace cpb
+
+// ---------------------------------------------------------------------------
+// Device-side P5 heatmap (field_io.py:138-150): gray = round(255 * clip(p, 0, 1)^gamma)
+// (numpy round-half-even), 0 where the pixel is invalid.
+// ---------------------------------------------------------------------------
+namespace cpb {
+namespace {
+__global__ void heatmap_kernel(const double* p, const uint8_t* valid, int64_t n, double gamma,
+                               uint8_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double x = fmin(fmax(p[i], 0.0), 1.0);
+  double y;
+  if (gamma == 1.0) y = x;                 // numpy's power fast paths
+  else if (gamma == 0.5) y = __dsqrt_rn(x);
+  else if (gamma == 2.0) y = __dmul_rn(x, x);
+  else y = pow(x, gamma);
+  const double g = rint(__dmul_rn(255.0, y));
+  out[i] = (valid && !valid[i]) ? (uint8_t)0 : (uint8_t)g;
+}
+}  // namespace
+
+int launch_heatmap(const double* p, const uint8_t* valid, int64_t n, double gamma, uint8_t* out,
+                   cudaStream_t st) {
+  if (n == 0) return CPB_OK;
+  heatmap_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, valid, n, gamma, out);
+  CPB_CHECK_LAUNCH("heatmap kernel");
+  return CPB_OK;
+}
+}  // namespace cpb

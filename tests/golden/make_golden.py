@@ -148,6 +148,30 @@ def main() -> None:
         rng_fx[f"{seed}"] = rngstream.unit_block(seed, px, 3, 11)
     rng_fx["pixels"] = px
 
+    # field_io: UCVF bytes, P5 heatmaps, CSV (field_io.py:35-150)
+    import tempfile
+
+    from critprob import field_io as fio
+
+    io_fx = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        stack = EnsembleStack(ens["ackley"])
+        fio.save_ensemble(stack, os.path.join(tmp, "e.ucvf"))
+        io_fx["ensemble_ucvf"] = np.frombuffer(open(os.path.join(tmp, "e.ucvf"), "rb").read(), np.uint8)
+        field = UncertainField.from_ensemble(stack, ModelSpec("uniform"))
+        prob = classify_field(field)
+        fio.save_probability_field(prob, os.path.join(tmp, "p.ucvf"))
+        io_fx["prob_ucvf"] = np.frombuffer(open(os.path.join(tmp, "p.ucvf"), "rb").read(), np.uint8)
+        fio.save_probability_field(prob, os.path.join(tmp, "p.csv"), format="csv")
+        io_fx["prob_csv"] = np.frombuffer(open(os.path.join(tmp, "p.csv"), "rb").read(), np.uint8)
+        for ch in ("min", "max", "saddle"):
+            io_fx[f"prob/{ch}"] = prob.channel(ch)
+            for g in (1.0, 0.5, 2.2):
+                fio.export_heatmap(prob, ch, os.path.join(tmp, "h.pgm"), gamma=g)
+                io_fx[f"heat/{ch}/{g}"] = np.frombuffer(open(os.path.join(tmp, "h.pgm"), "rb").read(), np.uint8)
+        io_fx["prob/valid"] = prob.valid
+    np.savez_compressed(os.path.join(HERE, "io.npz"), **io_fx)
+
     np.savez_compressed(os.path.join(HERE, "fit.npz"), **fit)
     np.savez_compressed(os.path.join(HERE, "closed.npz"), **closed)
     np.savez_compressed(os.path.join(HERE, "mc.npz"), **mc)
