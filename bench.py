@@ -261,7 +261,7 @@ def run_ours(args):
             name = f"fit_tma_kernel<{kind}>"
         else:
             nbytes = st_verts * (param_bytes(kind, bins) + 24)
-            name = {"uniform": "closed_uniform_kernel", "epanechnikov": "closed_epan_kernel",
+            name = {"uniform": "closed_uniform_kernel", "epanechnikov": "closed_pp_kernel<epanechnikov>",
                     "histogram": "closed_hist_tab_kernel"}[kind]
         kern[(kind, what)] = {"kernel": name, "ms": t, "bytes": nbytes, "gbs": nbytes / (t / 1e3) / 1e9}
     dom = max(kern.values(), key=lambda r: r["ms"])
