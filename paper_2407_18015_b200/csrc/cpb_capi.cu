@@ -34,6 +34,7 @@ int launch_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end,
                          double* pmax, double* psad, cudaStream_t st);
 int launch_heatmap(const double* p, const uint8_t* valid, int64_t n, double gamma, uint8_t* out,
                    cudaStream_t st);
+int launch_eps_sensitive_rows(const cpb_field* f, double eps, uint8_t* sens, cudaStream_t st);
 
 extern int g_fit_ctas_per_sm;
 
@@ -329,26 +330,38 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
   int s;
   for (int i = 0; i < nm; ++i)
     if ((s = cpb_field_plane_bytes(kinds[i], bins[i], (int32_t)members, height, width, pb[i]))) return s;
-  Streams ss;  // s[0], s[1]: chunk ring (H2D + fits); s[0] then also classifies
-  cudaStream_t scopy = nullptr;
-  cudaError_t e = cudaStreamCreateWithFlags(&scopy, cudaStreamNonBlocking);
+  // streams: ss.s[0..1] chunk ring (H2D + fits), sx[0] stencils, sx[1] D2H
+  Streams ss, sx;
+  cudaError_t e = cudaSuccess;
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     e = cudaStreamCreateWithFlags(&ss.s[i], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ss.ev[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&sx.s[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&sx.ev[i], cudaEventDisableTiming);
   }
   if (e != cudaSuccess) return cuda_status(e, "stream setup");
-  struct CopyStream {
-    cudaStream_t s;
-    ~CopyStream() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
-  } copy_guard{scopy};
-  cudaStream_t s0 = ss.s[0];
+  cudaStream_t s0 = ss.s[0], scls = sx.s[0], scopy = sx.s[1];
   const size_t plane = (size_t)height * width;
-  // per-model compact planes
-  DevBuf planes[16][7];
+  const size_t row_bytes = (size_t)members * width * sizeof(float);
+  static const size_t chunk_bytes = [] {  // CPB_HOST_CHUNK_BYTES overrides, for tests
+    const char* v = getenv("CPB_HOST_CHUNK_BYTES");
+    return v ? (size_t)atoll(v) : (size_t)(256u << 20);
+  }();
+  int64_t chunk = (int64_t)std::max<size_t>(2, chunk_bytes / row_bytes);
+  if (chunk > height) chunk = height;
+  const int64_t nchunks = (height + chunk - 1) / chunk;
+  // per-model compact planes, the device eps of every chunk, outputs
+  DevBuf planes[16][7], epsbuf[16], pair[16], out[16], sens[16];
   cpb_field fm[16];
   for (int i = 0; i < nm; ++i) {
     for (int q = 0; q < 7; ++q)
       if ((s = planes[i][q].alloc(pb[i][q], s0))) return s;
+    if ((s = epsbuf[i].alloc((size_t)nchunks * sizeof(double), s0)) ||
+        (s = pair[i].alloc(2 * sizeof(double), s0)) || (s = sens[i].alloc((size_t)height, s0)) ||
+        (s = out[i].alloc(3 * plane * sizeof(double), s0)))
+      return s;
+    e = cudaMemsetAsync(out[i].p, 0, 3 * plane * sizeof(double), s0);
+    if (e != cudaSuccess) return cuda_status(e, "memset");
     cpb_field& f = fm[i];
     f = cpb_field{};
     f.kind = kinds[i]; f.bins = bins[i]; f.members = (int32_t)members;
@@ -358,51 +371,67 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     f.spread = (double*)planes[i][3].p; f.weights = planes[i][4].p;
     f.weight_table = (double*)planes[i][5].p;
   }
-  // ping-pong output planes so the D2H of one model overlaps the next stencil
-  DevBuf out[2];
-  cudaEvent_t copied[2] = {nullptr, nullptr}, computed[2] = {nullptr, nullptr};
-  struct Events {  // destroyed before `out`: drains the copy stream before the buffers go
-    cudaEvent_t* a; cudaEvent_t* b; cudaStream_t cs;
-    ~Events() {
-      if (cs) cudaStreamSynchronize(cs);
-      for (int i = 0; i < 2; ++i) { if (a[i]) cudaEventDestroy(a[i]); if (b[i]) cudaEventDestroy(b[i]); }
-    }
-  } ev_guard{copied, computed, scopy};
-  for (int i = 0; i < 2; ++i) {
-    if ((s = out[i].alloc(3 * plane * sizeof(double), s0))) return s;
-    e = cudaMemsetAsync(out[i].p, 0, 3 * plane * sizeof(double), s0);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&computed[i], cudaEventDisableTiming);
-    if (e != cudaSuccess) return cuda_status(e, "output setup");
-  }
-  // row chunks of the ensemble, double-buffered: the H2D of chunk j+1 overlaps the
-  // fits of chunk j; each chunk is fitted for every model while it is resident
-  const size_t row_bytes = (size_t)members * width * sizeof(float);
-  // chunk bytes (CPB_HOST_CHUNK_BYTES overrides, for tests of the chunked path)
-  static const size_t chunk_bytes = [] {
-    const char* e = getenv("CPB_HOST_CHUNK_BYTES");
-    return e ? (size_t)atoll(e) : (size_t)(256u << 20);
-  }();
-  int64_t chunk = (int64_t)std::max<size_t>(1, chunk_bytes / row_bytes);
-  if (chunk > height) chunk = height;
   DevBuf ebuf[2];
   for (int i = 0; i < 2; ++i)
     if ((s = ebuf[i].alloc((size_t)chunk * row_bytes, s0))) return s;
   e = cudaEventRecord(ss.ev[0], s0);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.s[1], ss.ev[0], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(scls, ss.ev[0], 0);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(scopy, ss.ev[0], 0);
   if (e != cudaSuccess) return cuda_status(e, "event");
-  int nchunks = 0;
-  for (int64_t r0 = 0; r0 < height; r0 += chunk, ++nchunks) {
-    const int64_t nr = std::min(chunk, height - r0);
-    const int b = nchunks & 1;
+  struct Launch { int64_t r0, r1, chunk; };
+  std::vector<Launch> launches;
+  // per-chunk events (the ring events are reused, so the stencil stream waits on its own copy)
+  std::vector<cudaEvent_t> fitted((size_t)nchunks, nullptr), classified((size_t)nchunks, nullptr);
+  struct EvVec {
+    std::vector<cudaEvent_t>* a; std::vector<cudaEvent_t>* b; cudaStream_t c1, c2;
+    ~EvVec() {  // destroyed before the buffers: drain the stencil and copy streams first
+      if (c1) cudaStreamSynchronize(c1);
+      if (c2) cudaStreamSynchronize(c2);
+      for (auto* v : {a, b})
+        for (auto ev : *v) if (ev) cudaEventDestroy(ev);
+    }
+  } evguard{&fitted, &classified, scls, scopy};
+  for (int64_t j = 0; j < nchunks; ++j) {
+    e = cudaEventCreateWithFlags(&fitted[j], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&classified[j], cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e, "event create");
+  }
+  auto classify_rows = [&](int i, int64_t r0, int64_t r1, const double* eps_dev, double eps_host,
+                           cudaStream_t st) -> int {
+    cpb_field f = fm[i];
+    f.eps_device = eps_dev;
+    f.eps = eps_host;
+    double* pmin = (double*)out[i].p;
+    double* om = (channels & CPB_CH_MIN) ? pmin : nullptr;
+    double* oM = (channels & CPB_CH_MAX) ? pmin + plane : nullptr;
+    double* oS = (channels & CPB_CH_SADDLE) ? pmin + 2 * plane : nullptr;
+    if (method == 0) return cpb_classify_closed(&f, r0, r1, om, oM, oS, st);
+    return cpb_classify_mc(&f, r0, r1, seed, n_samples, CPB_RNG_SPLITMIX, om, oM, oS, nullptr, st);
+  };
+  auto copy_rows = [&](int i, int64_t r0, int64_t r1) -> int {
+    const double* base = (const double*)out[i].p;
+    for (int c = 0; c < 3; ++c) {
+      double* dst = h_out ? h_out[3 * i + c] : nullptr;
+      if (!dst || r1 <= r0) continue;
+      const size_t off = (size_t)r0 * width, n = (size_t)(r1 - r0) * width;
+      cudaError_t ce = cudaMemcpyAsync(dst + off, base + c * plane + off, n * sizeof(double),
+                                       cudaMemcpyDeviceToHost, scopy);
+      if (ce != cudaSuccess) return cuda_status(ce, "D2H probabilities");
+    }
+    return CPB_OK;
+  };
+  int64_t next_row = 1;  // first vertex row not yet classified
+  for (int64_t j = 0; j < nchunks; ++j) {
+    const int64_t r0 = j * chunk, nr = std::min(chunk, height - r0);
+    const int b = (int)(j & 1);
     cudaStream_t st = ss.s[b];
     // one 2-D copy: M member rows of nr*W floats, source pitch = member plane
     e = cudaMemcpy2DAsync(ebuf[b].p, (size_t)nr * width * sizeof(float), h_ens + r0 * width,
                           plane * sizeof(float), (size_t)nr * width * sizeof(float), (size_t)members,
                           cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_status(e, "H2D ensemble chunk");
-    // range accumulation is serialised across the two streams by the chunk order
-    if (nchunks > 0) {
+    if (j > 0) {  // range accumulation is serialised across the ring by chunk order
       e = cudaStreamWaitEvent(st, ss.ev[b ^ 1], 0);
       if (e != cudaSuccess) return cuda_status(e, "event wait");
     }
@@ -419,48 +448,71 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
       fc.weights = pb[i][4] ? (char*)planes[i][4].p + off * (members <= 255 ? 1 : 2) : nullptr;
       fc.plane_stride = (int64_t)plane;
       if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc,
-                       (uint32_t*)planes[i][6].p, nchunks > 0, st)))
+                       (uint32_t*)planes[i][6].p, j > 0, st)))
         return s;
       fm[i].bounds = fc.bounds;
       fm[i].weights_mode = fc.weights_mode;
+      // provisional eps of the rows fitted so far (exact once the last chunk is in)
+      if ((s = cpb_range_to_pair((const uint32_t*)planes[i][6].p, (double*)pair[i].p, st)) ||
+          (s = cpb_pair_to_eps((const double*)pair[i].p, (double*)epsbuf[i].p + j, st)))
+        return s;
     }
-    e = cudaEventRecord(ss.ev[b], st);
-    if (e != cudaSuccess) return cuda_status(e, "event record");
-  }
-  e = cudaStreamWaitEvent(s0, ss.ev[(nchunks - 1) & 1], 0);
-  if (e != cudaSuccess) return cuda_status(e, "event wait");
-  for (int i = 0; i < nm; ++i) {
-    double gmin = 0.0, gmax = 0.0;
-    if ((s = cpb_read_range((const uint32_t*)planes[i][6].p, &gmin, &gmax, s0))) return s;
-    fm[i].eps = cpb_epsilon(gmin, gmax);
-    const int o = i & 1;
-    if (i >= 2) {  // the D2H of model i-2 must be done with this buffer
-      e = cudaStreamWaitEvent(s0, copied[o], 0);
+    if ((e = cudaEventRecord(ss.ev[b], st)) != cudaSuccess || (e = cudaEventRecord(fitted[j], st)) != cudaSuccess)
+      return cuda_status(e, "event record");
+    // stencil the vertex rows whose three rows are now fitted, copy them back
+    const int64_t hi_row = (j + 1 == nchunks) ? height - 1 : std::min(r0 + nr - 1, height - 1);
+    if (hi_row > next_row) {
+      e = cudaStreamWaitEvent(scls, fitted[j], 0);
       if (e != cudaSuccess) return cuda_status(e, "event wait");
+      for (int i = 0; i < nm; ++i)
+        if ((s = classify_rows(i, next_row, hi_row, (const double*)epsbuf[i].p + j, 0.0, scls))) return s;
+      launches.push_back({next_row, hi_row, j});
+      if ((e = cudaEventRecord(classified[j], scls)) != cudaSuccess ||
+          (e = cudaStreamWaitEvent(scopy, classified[j], 0)) != cudaSuccess)
+        return cuda_status(e, "event");
+      for (int i = 0; i < nm; ++i)
+        if ((s = copy_rows(i, next_row, hi_row))) return s;
+      next_row = hi_row;
     }
-    double* pmin = (double*)out[o].p;
-    double* pmax = pmin + plane;
-    double* psad = pmax + plane;
-    double* om = (channels & CPB_CH_MIN) ? pmin : nullptr;
-    double* oM = (channels & CPB_CH_MAX) ? pmax : nullptr;
-    double* oS = (channels & CPB_CH_SADDLE) ? psad : nullptr;
-    if (method == 0)
-      s = cpb_classify_closed(&fm[i], 1, height - 1, om, oM, oS, s0);
-    else
-      s = cpb_classify_mc(&fm[i], 1, height - 1, seed, n_samples, CPB_RNG_SPLITMIX, om, oM, oS,
-                          nullptr, s0);
-    if (s) return s;
-    e = cudaEventRecord(computed[o], s0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(scopy, computed[o], 0);
-    if (e != cudaSuccess) return cuda_status(e, "event");
-    for (int c = 0; c < 3; ++c) {
-      double* dst = h_out ? h_out[3 * i + c] : nullptr;
-      if (!dst) continue;
-      e = cudaMemcpyAsync(dst, pmin + c * plane, plane * sizeof(double), cudaMemcpyDeviceToHost, scopy);
-      if (e != cudaSuccess) return cuda_status(e, "D2H probabilities");
+  }
+  // exactness: rows stencilled with a provisional eps are redone where some
+  // pixel's result depends on eps (degenerate / clamped pixels; normally none)
+  e = cudaStreamSynchronize(ss.s[0]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ss.s[1]);
+  if (e != cudaSuccess) return cuda_status(e, "synchronize");
+  std::vector<double> eps_host((size_t)nchunks);
+  std::vector<uint8_t> sens_host((size_t)height);
+  for (int i = 0; i < nm; ++i) {
+    e = cudaMemcpy(eps_host.data(), epsbuf[i].p, (size_t)nchunks * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_status(e, "D2H eps");
+    const double eps_final = eps_host[(size_t)nchunks - 1];
+    if (eps_final != eps_final) { set_error("ensemble values must be finite"); return CPB_ENONFINITE; }
+    fm[i].eps = eps_final;
+    bool stale = false;
+    for (const Launch& L : launches) stale |= eps_host[(size_t)L.chunk] != eps_final;
+    if (!stale) continue;
+    if ((s = launch_eps_sensitive_rows(&fm[i], eps_final, (uint8_t*)sens[i].p, scls))) return s;
+    e = cudaMemcpyAsync(sens_host.data(), sens[i].p, (size_t)height, cudaMemcpyDeviceToHost, scls);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(scls);
+    if (e != cudaSuccess) return cuda_status(e, "D2H sensitivity");
+    for (const Launch& L : launches) {
+      if (eps_host[(size_t)L.chunk] == eps_final) continue;
+      for (int64_t v = L.r0; v < L.r1;) {
+        if (!(sens_host[v - 1] | sens_host[v] | sens_host[v + 1])) { ++v; continue; }
+        int64_t w = v + 1;
+        while (w < L.r1 && (sens_host[w - 1] | sens_host[w] | sens_host[w + 1])) ++w;
+        if ((s = classify_rows(i, v, w, nullptr, eps_final, scls))) return s;
+        cudaEvent_t done;
+        if ((e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming)) != cudaSuccess)
+          return cuda_status(e, "event");
+        e = cudaEventRecord(done, scls);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(scopy, done, 0);
+        cudaEventDestroy(done);
+        if (e != cudaSuccess) return cuda_status(e, "event");
+        if ((s = copy_rows(i, v, w))) return s;
+        v = w;
+      }
     }
-    e = cudaEventRecord(copied[o], scopy);
-    if (e != cudaSuccess) return cuda_status(e, "event record");
   }
   if (h_valid) {
     for (int64_t r = 0; r < height; ++r) {
@@ -471,8 +523,8 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
       row[width - 1] = 0;
     }
   }
-  e = cudaStreamSynchronize(scopy);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s0);
+  e = cudaStreamSynchronize(scls);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(scopy);
   if (e != cudaSuccess) return cuda_status(e, "synchronize");
   return CPB_OK;
 }

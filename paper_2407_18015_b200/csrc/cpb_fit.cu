@@ -818,3 +818,36 @@ int launch_heatmap(const double* p, const uint8_t* valid, int64_t n, double gamm
   return CPB_OK;
 }
 }  // namespace cpb
+
+// ---------------------------------------------------------------------------
+// Rows whose stencil results depend on eps (for streamed classification with
+// a provisional eps): sens[r] = 1 if row r holds a fitted uniform/histogram
+// pixel with hi <= lo (widened by eps/2 at use, fields.py:140-143) or an
+// Epanechnikov pixel with k * std < eps / 2 (clamped at use, fields.py:156).
+// ---------------------------------------------------------------------------
+namespace cpb {
+namespace {
+__global__ void eps_sensitive_rows_kernel(FieldView f, double eps, uint8_t* sens) {
+  const int64_t r = blockIdx.x;
+  int any = 0;
+  for (int64_t c = threadIdx.x; c < f.width; c += blockDim.x) {
+    const int64_t i = r * f.width + c;
+    if (f.kind == CPB_EPANECHNIKOV) {
+      any |= __dmul_rn(f.k, f.spread[i]) < __dmul_rn(0.5, eps);
+    } else if (f.kind != CPB_GAUSSIAN && f.bounds == CPB_BOUNDS_F32_FITTED) {
+      any |= static_cast<const float*>(f.hi)[i] <= static_cast<const float*>(f.lo)[i];
+    }
+  }
+  any = __syncthreads_or(any);
+  if (threadIdx.x == 0) sens[r] = (uint8_t)(any ? 1 : 0);
+}
+}  // namespace
+
+int launch_eps_sensitive_rows(const cpb_field* fld, double eps, uint8_t* sens, cudaStream_t st) {
+  const FieldView f = make_view(*fld);
+  if (f.height == 0) return CPB_OK;
+  eps_sensitive_rows_kernel<<<(unsigned)f.height, 256, 0, st>>>(f, eps, sens);
+  CPB_CHECK_LAUNCH("eps sensitivity kernel");
+  return CPB_OK;
+}
+}  // namespace cpb

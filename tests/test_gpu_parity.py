@@ -417,3 +417,32 @@ def test_combinatorial_against_reference(golden):
     assert seen >= 8
     with pytest.raises(ValueError):
         cpb.classify_field(_fit(fit["ens/rand"], "histogram", 9), cpb.EstimatorSpec(method="combinatorial"))
+
+
+def test_run_host_streaming_eps_fixup():
+    """Chunks are stencilled with a provisional eps; rows whose pixels depend on
+    eps (degenerate / clamped) are redone once the last chunk sets the global eps."""
+    import ctypes
+
+    from paper_2407_18015_b200 import _lib
+
+    lib = _lib.load()
+    rng = np.random.default_rng(8)
+    M, H, W = 6, 300, 20
+    vals = (rng.uniform(-1, 1, (H, W)) + rng.uniform(-0.3, 0.3, (M, H, W))).astype(np.float32)
+    vals[:, 5, 7] = 0.25          # degenerate pixel in the first chunk
+    vals[:, 6, 3] = vals[0, 6, 3]  # and another (epanechnikov: std == 0 -> clamped to eps/2)
+    vals[2, 280, 11] = 1000.0     # the last chunk widens the global range, hence eps
+    vals = np.ascontiguousarray(vals)
+    models = [("uniform", 5), ("epanechnikov", 5), ("histogram", 3)]
+    outs = [np.zeros((H, W)) for _ in range(9)]
+    kinds = (ctypes.c_int32 * 3)(*[_lib.KIND_CODES[k] for k, _ in models])
+    bins = (ctypes.c_int32 * 3)(*[b for _, b in models])
+    ks = (ctypes.c_double * 3)(*[float(cpb.ModelSpec(k).k) for k, _ in models])
+    ptrs = (ctypes.c_void_p * 9)(*[o.ctypes.data for o in outs])
+    _lib.check(lib.cpb_run_host_models(vals.ctypes.data, M, H, W, 3, kinds, bins, ks, 0, 0, 0, 7,
+                                       ptrs, None))
+    for i, (kind, b) in enumerate(models):
+        ref = orc.classify(orc.fit(vals, kind, b), kind)
+        for c, ch in enumerate(("min", "max", "saddle")):
+            assert np.max(np.abs(outs[3 * i + c] - ref[ch])) <= CLOSED_TOL, (kind, ch)
