@@ -246,9 +246,14 @@ int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t wi
  * Several models over ONE upload of the ensemble (the reference workflow
  * `stack = EnsembleStack(v); for model: classify_field(from_ensemble(stack,
  * model))`): every row chunk crossing PCIe is fitted for all n_models models
- * while resident; then each model is classified and its planes copied back
- * while the next model's stencil runs.  Model i is (kinds[i], bins[i], ks[i]);
- * h_out[3*i + c] receives channel c (min, max, saddle) of model i (NULL skips).
+ * while resident, and the vertex rows a chunk completes are stencilled and
+ * copied back while later chunks are still crossing PCIe (the eps of the rows
+ * seen so far is kept on the device; rows whose result depends on eps are
+ * redone with the final eps, so the output equals the whole-stack result).
+ * Model i is (kinds[i], bins[i], ks[i]); h_out[3*i + c] receives channel c
+ * (min, max, saddle) of model i (NULL skips).  Device scratch comes from a
+ * library-owned stream-ordered pool that keeps its memory between calls
+ * (see cpb_release_workspace).
  */
 int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int64_t width,
                         int32_t n_models, const int32_t* kinds, const int32_t* bins,
@@ -264,6 +269,10 @@ int cpb_heatmap(const double* d_p, const uint8_t* d_valid, int64_t n, double gam
 /* Pinned host memory for cpb_run_host buffers. */
 int cpb_host_alloc(void** ptr, size_t bytes);
 int cpb_host_free(void* ptr);
+
+/* Return the current device's cached workspace (the pool cpb_run_host* draw
+ * their device scratch from) to the driver.  Reports the bytes released. */
+int cpb_release_workspace(size_t* released_bytes);
 
 #ifdef __cplusplus
 }

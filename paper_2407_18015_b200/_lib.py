@@ -67,6 +67,7 @@ _SIGNATURES = {
     "cpb_heatmap": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
     "cpb_host_alloc": (c_i32, [ctypes.POINTER(c_vp), ctypes.c_size_t]),
     "cpb_host_free": (c_i32, [c_vp]),
+    "cpb_release_workspace": (c_i32, [ctypes.POINTER(ctypes.c_size_t)]),
 }
 
 EXPORTED = tuple(_SIGNATURES)

@@ -7,6 +7,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <mutex>
+#include <chrono>
 #include <vector>
 
 #include "cpb_common.cuh"
@@ -279,6 +281,34 @@ int cpb_host_free(void* ptr) {
 // ---------------------------------------------------------------------------
 namespace {
 
+// Library-owned stream-ordered pool per device.  Its release threshold is
+// unbounded, so a host call's multi-GB scratch stays mapped for the next call:
+// with the default pool every call re-maps (and at the final synchronize
+// unmaps) tens of GB, which costs 0.1-3 s of host time per call.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+
+int workspace_pool(cudaMemPool_t* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  if (dev < 0 || dev >= 64) { set_error("device ordinal out of range"); return CPB_EINVAL; }
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (!g_pool[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    e = cudaMemPoolCreate(&g_pool[dev], &props);
+    if (e != cudaSuccess) { g_pool[dev] = nullptr; return cuda_status(e, "cudaMemPoolCreate"); }
+    uint64_t keep = ~0ull;
+    e = cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMemPoolSetAttribute");
+  }
+  *out = g_pool[dev];
+  return CPB_OK;
+}
+
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t st = nullptr;
@@ -288,7 +318,9 @@ struct DevBuf {
   int alloc(size_t bytes, cudaStream_t s) {
     st = s;
     if (bytes == 0) return CPB_OK;
-    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    cudaMemPool_t pool;
+    if (int rc = workspace_pool(&pool)) return rc;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, pool, s);
     if (e != cudaSuccess) { p = nullptr; return cuda_status(e, "cudaMallocAsync"); }
     return CPB_OK;
   }
@@ -326,6 +358,10 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     }
   }
   const int nm = n_models;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto host_ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  };
   size_t pb[16][7];
   int s;
   for (int i = 0; i < nm; ++i)
@@ -421,6 +457,18 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     }
     return CPB_OK;
   };
+  // CPB_HOST_TRACE=1: per-chunk timeline on stderr (H2D done, fits done, stencil done)
+  static const bool trace = getenv("CPB_HOST_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto tmark = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t ev;
+    cudaEventCreate(&ev);
+    cudaEventRecord(ev, st);
+    tev.push_back(ev);
+  };
+  tmark(s0);
+  const double t_setup = host_ms();
   int64_t next_row = 1;  // first vertex row not yet classified
   for (int64_t j = 0; j < nchunks; ++j) {
     const int64_t r0 = j * chunk, nr = std::min(chunk, height - r0);
@@ -431,6 +479,7 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
                           plane * sizeof(float), (size_t)nr * width * sizeof(float), (size_t)members,
                           cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_status(e, "H2D ensemble chunk");
+    tmark(st);
     if (j > 0) {  // range accumulation is serialised across the ring by chunk order
       e = cudaStreamWaitEvent(st, ss.ev[b ^ 1], 0);
       if (e != cudaSuccess) return cuda_status(e, "event wait");
@@ -459,6 +508,7 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     }
     if ((e = cudaEventRecord(ss.ev[b], st)) != cudaSuccess || (e = cudaEventRecord(fitted[j], st)) != cudaSuccess)
       return cuda_status(e, "event record");
+    tmark(st);
     // stencil the vertex rows whose three rows are now fitted, copy them back
     const int64_t hi_row = (j + 1 == nchunks) ? height - 1 : std::min(r0 + nr - 1, height - 1);
     if (hi_row > next_row) {
@@ -467,6 +517,7 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
       for (int i = 0; i < nm; ++i)
         if ((s = classify_rows(i, next_row, hi_row, (const double*)epsbuf[i].p + j, 0.0, scls))) return s;
       launches.push_back({next_row, hi_row, j});
+      tmark(scls);
       if ((e = cudaEventRecord(classified[j], scls)) != cudaSuccess ||
           (e = cudaStreamWaitEvent(scopy, classified[j], 0)) != cudaSuccess)
         return cuda_status(e, "event");
@@ -475,6 +526,7 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
       next_row = hi_row;
     }
   }
+  const double t_enqueued = host_ms();
   // exactness: rows stencilled with a provisional eps are redone where some
   // pixel's result depends on eps (degenerate / clamped pixels; normally none)
   e = cudaStreamSynchronize(ss.s[0]);
@@ -526,6 +578,28 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
   e = cudaStreamSynchronize(scls);
   if (e == cudaSuccess) e = cudaStreamSynchronize(scopy);
   if (e != cudaSuccess) return cuda_status(e, "synchronize");
+  if (trace) {
+    fprintf(stderr, "cpb_trace_host setup=%.1f enqueued=%.1f done=%.1f ms\n", t_setup, t_enqueued, host_ms());
+    for (size_t q = 1; q < tev.size(); ++q) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0], tev[q]);
+      fprintf(stderr, "%s%.2f", q == 1 ? "cpb_trace_ms " : " ", ms);
+    }
+    fprintf(stderr, "\n");
+    for (auto ev : tev) cudaEventDestroy(ev);
+  }
+  return CPB_OK;
+}
+
+int cpb_release_workspace(size_t* released_bytes) {
+  cudaMemPool_t pool;
+  if (int rc = workspace_pool(&pool)) return rc;
+  uint64_t before = 0, after = 0;
+  cudaError_t e = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &before);
+  if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+  if (e == cudaSuccess) e = cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &after);
+  if (e != cudaSuccess) return cuda_status(e, "cudaMemPoolTrimTo");
+  if (released_bytes) *released_bytes = (size_t)(before - after);
   return CPB_OK;
 }
 

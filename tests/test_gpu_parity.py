@@ -446,3 +446,20 @@ def test_run_host_streaming_eps_fixup():
         ref = orc.classify(orc.fit(vals, kind, b), kind)
         for c, ch in enumerate(("min", "max", "saddle")):
             assert np.max(np.abs(outs[3 * i + c] - ref[ch])) <= CLOSED_TOL, (kind, ch)
+
+
+def test_release_workspace_returns_cached_scratch():
+    import ctypes
+
+    from paper_2407_18015_b200 import _lib
+
+    lib = _lib.load()
+    vals = np.ascontiguousarray(orc.ackley_ensemble(40, 30, 8, noise_amp=0.3, seed=0))
+    outs = [np.zeros((30, 40)) for _ in range(3)]
+    _lib.check(lib.cpb_run_host(vals.ctypes.data, 8, 30, 40, _lib.KIND_CODES["uniform"], 5, 1.0, 0, 0,
+                                0, 7, *[o.ctypes.data for o in outs], None))
+    released = ctypes.c_size_t(0)
+    _lib.check(lib.cpb_release_workspace(ctypes.byref(released)))
+    assert released.value > 0
+    _lib.check(lib.cpb_release_workspace(ctypes.byref(released)))
+    assert released.value == 0
