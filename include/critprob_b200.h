@@ -14,6 +14,7 @@
  *   cpb_materialize      UncertainField.params             fields.py:86-103 (reference f64 layout)
  *   cpb_unit_block       rngstream.unit_block              rngstream.py:33-48
  *   cpb_run_host         from_ensemble + classify_field with host buffers (one call, H2D/D2H inside)
+ *   cpb_cases_*          the per-case API (NeighborhoodCase, engine.py:50-459) over a batch of cases
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  "d_" pointers are CUDA
@@ -265,6 +266,52 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
  * is 0 (d_valid may be NULL). */
 int cpb_heatmap(const double* d_p, const uint8_t* d_valid, int64_t n, double gamma,
                 uint8_t* d_out, void* stream);
+
+/*
+ * Batched per-case API.  A batch is n_cases neighbourhoods (NeighborhoodCase,
+ * engine.py:50-71), each a centre plus `neighbors` (2 or 4) distributions in
+ * the reference's order (east, north, west, south | first, second), stored
+ * position-major per case: distribution d = case * (1 + neighbors) + position.
+ * Kinds may be mixed inside a case.  All arrays are device memory.
+ *   uniform / epanechnikov / histogram : a = support lo, b = support hi
+ *                                        (epanechnikov(mean, hw) has support mean -+ hw)
+ *   gaussian (GaussianSampler)          : a = mean, b = stddev (Monte Carlo only)
+ *   histogram                           : bins[d] bins, weights[woff[d] + j], already
+ *                                         normalised (FiniteDistribution stores w / w.sum())
+ * Outputs are n_cases x 3 float64 (p_min, p_max, p_saddle) per case.
+ */
+typedef struct cpb_case_batch {
+  int64_t n_cases;
+  int32_t neighbors;       /* 2 or 4 */
+  int32_t max_bins;        /* largest histogram bin count in the batch (1 if none) */
+  const int32_t* kind;     /* CPB_UNIFORM | CPB_EPANECHNIKOV | CPB_HISTOGRAM | CPB_GAUSSIAN */
+  const double* a;
+  const double* b;
+  const int32_t* bins;
+  const int64_t* woff;
+  const double* weights;
+} cpb_case_batch;
+
+/* closed_form_triple (engine.py:177-178) of every case: exact piecewise
+ * integration on the breakpoint union.  Cases holding a Gaussian yield NaN
+ * (the reference raises TypeError; check kinds before calling). */
+int cpb_cases_closed(const cpb_case_batch* batch, double* d_out, void* stream);
+
+/* mc_all_patterns(case_i, n, seed, pixel_i) (engine.py:238-247) of every case:
+ * pixel_i = d_pixels[i] (NULL: i).  Bit-identical to the reference for
+ * uniform / histogram kinds.  d_counts (n_cases x 3 uint64, optional) receives
+ * the pattern counts. */
+int cpb_cases_mc(const cpb_case_batch* batch, uint64_t seed, const uint64_t* d_pixels, int64_t n,
+                 uint64_t* d_counts, double* d_out, void* stream);
+
+/* semianalytical_prob(case_i, pattern, c, seed, pixel_i) for all three patterns
+ * (engine.py:416-441); histogram-only cases (others yield NaN). */
+int cpb_cases_semi(const cpb_case_batch* batch, uint64_t seed, const uint64_t* d_pixels, int64_t c,
+                   double* d_out, void* stream);
+
+/* combinatorial_triple (engine.py:399-404, Eq. 5); histogram-only cases with
+ * at most 8 bins (CPB_EINVAL above, as the reference's ValueError). */
+int cpb_cases_combinatorial(const cpb_case_batch* batch, double* d_out, void* stream);
 
 /* Pinned host memory for cpb_run_host buffers. */
 int cpb_host_alloc(void** ptr, size_t bytes);

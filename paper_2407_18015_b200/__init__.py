@@ -7,6 +7,35 @@ closed-form min/max/saddle stencil and the Monte Carlo estimator
 the C ABI in include/critprob_b200.h.  There is no CPU fallback.
 """
 
+from .cases import (
+    CaseBatch,
+    FiniteDistribution,
+    GaussianSampler,
+    NeighborhoodCase,
+    ProbabilityTriple,
+    Support,
+    ValidationSummary,
+    case_at,
+    closed_form_triple,
+    closed_form_triples,
+    closed_pattern_prob,
+    combinatorial_batch,
+    combinatorial_triple,
+    epanechnikov,
+    histogram,
+    histogram_min_prob_combinatorial,
+    local_max_prob,
+    local_min_prob,
+    mc_all_patterns,
+    mc_all_patterns_batch,
+    mc_pattern_prob,
+    random_case,
+    saddle_prob,
+    semianalytical_batch,
+    semianalytical_prob,
+    uniform,
+    validate_random_cases,
+)
 from .engine import (
     COMBINATORIAL_MAX_BINS,
     ESTIMATOR_METHODS,
@@ -49,4 +78,11 @@ __all__ = [
     "UcvfValueError", "export_heatmap", "load_ensemble", "load_probability_field",
     "load_scalar_field", "save_ensemble", "save_probability_field", "save_scalar_field",
     "uniform_field_from_scalar",
+    # per-case API (engine.py:50-459) as GPU batches
+    "CaseBatch", "FiniteDistribution", "GaussianSampler", "NeighborhoodCase", "ProbabilityTriple",
+    "Support", "ValidationSummary", "case_at", "closed_form_triple", "closed_form_triples",
+    "closed_pattern_prob", "combinatorial_batch", "combinatorial_triple", "epanechnikov", "histogram",
+    "histogram_min_prob_combinatorial", "local_max_prob", "local_min_prob", "mc_all_patterns",
+    "mc_all_patterns_batch", "mc_pattern_prob", "random_case", "saddle_prob", "semianalytical_batch",
+    "semianalytical_prob", "uniform", "validate_random_cases",
 ]

@@ -38,6 +38,15 @@ class CpbField(ctypes.Structure):
     ]
 
 
+class CpbCaseBatch(ctypes.Structure):
+    """Mirror of `struct cpb_case_batch` (include/critprob_b200.h)."""
+
+    _fields_ = [
+        ("n_cases", c_i64), ("neighbors", c_i32), ("max_bins", c_i32),
+        ("kind", c_vp), ("a", c_vp), ("b", c_vp), ("bins", c_vp), ("woff", c_vp), ("weights", c_vp),
+    ]
+
+
 _SIGNATURES = {
     "cpb_abi_version": (c_i32, []),
     "cpb_last_error": (ctypes.c_char_p, []),
@@ -65,6 +74,10 @@ _SIGNATURES = {
                                     ctypes.POINTER(c_i32), ctypes.POINTER(c_dbl), c_i32, c_u64,
                                     c_i64, c_u32, ctypes.POINTER(c_vp), c_vp]),
     "cpb_heatmap": (c_i32, [c_vp, c_vp, c_i64, c_dbl, c_vp, c_vp]),
+    "cpb_cases_closed": (c_i32, [ctypes.POINTER(CpbCaseBatch), c_vp, c_vp]),
+    "cpb_cases_mc": (c_i32, [ctypes.POINTER(CpbCaseBatch), c_u64, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "cpb_cases_semi": (c_i32, [ctypes.POINTER(CpbCaseBatch), c_u64, c_vp, c_i64, c_vp, c_vp]),
+    "cpb_cases_combinatorial": (c_i32, [ctypes.POINTER(CpbCaseBatch), c_vp, c_vp]),
     "cpb_host_alloc": (c_i32, [ctypes.POINTER(c_vp), ctypes.c_size_t]),
     "cpb_host_free": (c_i32, [c_vp]),
     "cpb_release_workspace": (c_i32, [ctypes.POINTER(ctypes.c_size_t)]),

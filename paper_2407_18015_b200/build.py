@@ -26,6 +26,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-
 UNITS = {
     "cpb_fit.cu": ["-fmad=false"],
     "cpb_mc.cu": ["-fmad=false"],
+    "cpb_cases.cu": ["-fmad=false"],
     "cpb_closed.cu": [],
     "cpb_capi.cu": [],
 }

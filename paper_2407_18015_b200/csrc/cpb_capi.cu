@@ -37,6 +37,12 @@ int launch_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end,
 int launch_heatmap(const double* p, const uint8_t* valid, int64_t n, double gamma, uint8_t* out,
                    cudaStream_t st);
 int launch_eps_sensitive_rows(const cpb_field* f, double eps, uint8_t* sens, cudaStream_t st);
+int launch_cases_closed(const cpb_case_batch* b, double* out, cudaStream_t st);
+int launch_cases_mc(const cpb_case_batch* b, uint64_t seed, const uint64_t* pixels, int64_t n,
+                    unsigned long long* counts, double* out, cudaStream_t st);
+int launch_cases_semi(const cpb_case_batch* b, uint64_t seed, const uint64_t* pixels, int64_t c,
+                      double* out, cudaStream_t st);
+int launch_cases_combinatorial(const cpb_case_batch* b, double* out, cudaStream_t st);
 
 extern int g_fit_ctas_per_sm;
 
@@ -308,6 +314,22 @@ int workspace_pool(cudaMemPool_t* out) {
   *out = g_pool[dev];
   return CPB_OK;
 }
+
+}  // namespace
+
+int workspace_alloc(void** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool;
+  if (int rc = workspace_pool(&pool)) return rc;
+  cudaError_t e = cudaMallocFromPoolAsync(p, bytes, pool, st);
+  if (e != cudaSuccess) { *p = nullptr; return cuda_status(e, "cudaMallocFromPoolAsync"); }
+  return CPB_OK;
+}
+
+void workspace_free(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+namespace {
 
 struct DevBuf {
   void* p = nullptr;
@@ -589,6 +611,25 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     for (auto ev : tev) cudaEventDestroy(ev);
   }
   return CPB_OK;
+}
+
+int cpb_cases_closed(const cpb_case_batch* batch, double* d_out, void* stream) {
+  return launch_cases_closed(batch, d_out, (cudaStream_t)stream);
+}
+
+int cpb_cases_mc(const cpb_case_batch* batch, uint64_t seed, const uint64_t* d_pixels, int64_t n,
+                 uint64_t* d_counts, double* d_out, void* stream) {
+  return launch_cases_mc(batch, seed, d_pixels, n, (unsigned long long*)d_counts, d_out,
+                         (cudaStream_t)stream);
+}
+
+int cpb_cases_semi(const cpb_case_batch* batch, uint64_t seed, const uint64_t* d_pixels, int64_t c,
+                   double* d_out, void* stream) {
+  return launch_cases_semi(batch, seed, d_pixels, c, d_out, (cudaStream_t)stream);
+}
+
+int cpb_cases_combinatorial(const cpb_case_batch* batch, double* d_out, void* stream) {
+  return launch_cases_combinatorial(batch, d_out, (cudaStream_t)stream);
 }
 
 int cpb_release_workspace(size_t* released_bytes) {

@@ -15,6 +15,7 @@
 // (log1p/cos) draws can differ from glibc by an ulp, which flips a strict
 // comparison only on an exact tie.
 #include "cpb_common.cuh"
+#include "cpb_sample.cuh"
 
 namespace cpb {
 namespace {
@@ -30,37 +31,6 @@ struct McArgs {
   double* psad;
   int64_t* counts;  // optional: 3 planes (min, max, saddle)
 };
-
-// Per-position sampler state (histogram tables live in shared memory).
-struct Sampler {
-  double a, b;      // uniform: lo, hi | epanechnikov: mid, half | gaussian: mean, sd | histogram: lo, binw
-  const double* wn; // histogram: h renormalised weights (smem)
-  const double* cum;// histogram: h+1 prefix sums, cum[h] = 1 (smem)
-};
-
-template <int KIND>
-CPB_D double draw(const Sampler& s, double u, double u2, int h) {
-  if (KIND == CPB_UNIFORM) {  // (1 - u) lo + u hi  (distributions.py:60-61)
-    return __dadd_rn(__dmul_rn(__dsub_rn(1.0, u), s.a), __dmul_rn(u, s.b));
-  } else if (KIND == CPB_EPANECHNIKOV) {  // distributions.py:64-70
-    if (u == 0.0) return __dsub_rn(s.a, s.b);
-    if (u == 1.0) return __dadd_rn(s.a, s.b);
-    const double root = __dmul_rn(2.0, sin(__ddiv_rn(asin(__dsub_rn(__dmul_rn(2.0, u), 1.0)), 3.0)));
-    return __dadd_rn(s.a, __dmul_rn(s.b, root));
-  } else if (KIND == CPB_GAUSSIAN) {  // Box-Muller, engine.py:638-640
-    const double r = __dsqrt_rn(__dmul_rn(-2.0, log1p(-u)));
-    const double z = __dmul_rn(r, cos(__dmul_rn(6.283185307179586, u2)));
-    return __dadd_rn(s.a, __dmul_rn(s.b, z));
-  } else {  // histogram_icdf, distributions.py:73-89
-    int j = 0;
-    for (int k = 1; k < h; ++k) j += (u >= s.cum[k]) ? 1 : 0;
-    const double cj = s.cum[j], wj = s.wn[j];
-    const double frac = wj > 0.0 ? __ddiv_rn(__dsub_rn(u, cj), wj) : 0.0;
-    if (u == 1.0) return __dadd_rn(s.a, __dmul_rn(s.b, (double)h));
-    const double e0 = __dadd_rn(s.a, __dmul_rn(s.b, (double)j));
-    return __dadd_rn(__dmul_rn(__dsub_rn(1.0, frac), e0), __dmul_rn(frac, __dadd_rn(e0, s.b)));
-  }
-}
 
 template <int KIND, int RNG>
 __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a) {
@@ -178,15 +148,6 @@ __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a
 // One warp per vertex; lanes accumulate float64 partial sums over a strided
 // subset of the draws and a fixed-shape warp tree adds them, so the result is
 // deterministic (it re-associates numpy's pairwise mean: ~1e-16 relative).
-CPB_D double hist_cdf_at(const double* wn, const double* cum, double lo, double binw, int h,
-                         double x) {
-  double t = floor(__ddiv_rn(__dsub_rn(x, lo), binw));
-  const int j = (int)fmax(0.0, fmin(t, (double)(h - 1)));
-  const double frac = __ddiv_rn(__dsub_rn(x, __dadd_rn(lo, __dmul_rn(binw, (double)j))), binw);
-  const double v = __dadd_rn(cum[j], __dmul_rn(wn[j], frac));
-  return fmin(fmax(v, 0.0), 1.0);
-}
-
 __global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs a) {
   extern __shared__ double s_tab[];  // per warp: 5 x (h wn + h+1 cum) + 1 x (h+1) centre cum
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -1,0 +1,55 @@
+// Inverse-CDF samplers and the histogram CDF lookup shared by the grid
+// Monte Carlo / semianalytical kernels (cpb_mc.cu) and the per-case batch
+// kernels (cpb_cases.cu).  Every operation is an explicit round-to-nearest
+// intrinsic so the draws repeat numpy's float64 arithmetic bit for bit
+// (distributions.py:60-100).
+#pragma once
+
+#include "cpb_common.cuh"
+
+namespace cpb {
+
+// Per-position sampler state (histogram tables live in shared memory).
+struct Sampler {
+  double a, b;      // uniform: lo, hi | epanechnikov: mid, half | gaussian: mean, sd | histogram: lo, binw
+  const double* wn; // histogram: h renormalised weights (smem)
+  const double* cum;// histogram: h+1 prefix sums, cum[h] = 1 (smem)
+};
+
+template <int KIND>
+CPB_D double draw(const Sampler& s, double u, double u2, int h) {
+  if (KIND == CPB_UNIFORM) {  // (1 - u) lo + u hi  (distributions.py:60-61)
+    return __dadd_rn(__dmul_rn(__dsub_rn(1.0, u), s.a), __dmul_rn(u, s.b));
+  } else if (KIND == CPB_EPANECHNIKOV) {  // distributions.py:64-70
+    if (u == 0.0) return __dsub_rn(s.a, s.b);
+    if (u == 1.0) return __dadd_rn(s.a, s.b);
+    const double root = __dmul_rn(2.0, sin(__ddiv_rn(asin(__dsub_rn(__dmul_rn(2.0, u), 1.0)), 3.0)));
+    return __dadd_rn(s.a, __dmul_rn(s.b, root));
+  } else if (KIND == CPB_GAUSSIAN) {  // Box-Muller, engine.py:638-640
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log1p(-u)));
+    const double z = __dmul_rn(r, cos(__dmul_rn(6.283185307179586, u2)));
+    return __dadd_rn(s.a, __dmul_rn(s.b, z));
+  } else {  // histogram_icdf, distributions.py:73-89
+    int j = 0;
+    for (int k = 1; k < h; ++k) j += (u >= s.cum[k]) ? 1 : 0;
+    const double cj = s.cum[j], wj = s.wn[j];
+    const double frac = wj > 0.0 ? __ddiv_rn(__dsub_rn(u, cj), wj) : 0.0;
+    if (u == 1.0) return __dadd_rn(s.a, __dmul_rn(s.b, (double)h));
+    const double e0 = __dadd_rn(s.a, __dmul_rn(s.b, (double)j));
+    return __dadd_rn(__dmul_rn(__dsub_rn(1.0, frac), e0), __dmul_rn(frac, __dadd_rn(e0, s.b)));
+  }
+}
+
+// Histogram CDF at x (histogram_cdf_values, distributions.py:92-100): bin
+// floor((x - lo) / binw) clipped to [0, h-1], cum[j] + wn[j] * frac, clipped
+// to [0, 1].
+CPB_D double hist_cdf_at(const double* wn, const double* cum, double lo, double binw, int h,
+                         double x) {
+  double t = floor(__ddiv_rn(__dsub_rn(x, lo), binw));
+  const int j = (int)fmax(0.0, fmin(t, (double)(h - 1)));
+  const double frac = __ddiv_rn(__dsub_rn(x, __dadd_rn(lo, __dmul_rn(binw, (double)j))), binw);
+  const double v = __dadd_rn(cum[j], __dmul_rn(wn[j], frac));
+  return fmin(fmax(v, 0.0), 1.0);
+}
+
+}  // namespace cpb

@@ -16,6 +16,9 @@ The fixtures travel with the repo; nothing at test time reads
 - classify_field semianalytical (engine.py:669-683)
 - classify_field combinatorial  (engine.py:686-702)
 - rngstream.unit_block          (rngstream.py:33-48)
+- per-case API over seeded random_case / mixed-kind cases (cases.npz):
+  closed_form_triple (engine.py:177), mc_all_patterns (238-247),
+  semianalytical_prob (416-441), combinatorial_triple (399-404)
 """
 
 from __future__ import annotations
@@ -29,9 +32,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from critprob import rngstream  # noqa: E402
-from critprob.engine import EstimatorSpec, classify_field  # noqa: E402
+from critprob.distributions import GaussianSampler, epanechnikov, histogram, uniform  # noqa: E402
+from critprob.engine import (  # noqa: E402
+    EstimatorSpec,
+    NeighborhoodCase,
+    classify_field,
+    closed_form_triple,
+    combinatorial_triple,
+    mc_all_patterns,
+    semianalytical_prob,
+)
 from critprob.fields import EnsembleStack, ModelSpec, UncertainField  # noqa: E402
-from critprob.synth import ackley_ensemble  # noqa: E402
+from critprob.synth import ackley_ensemble, random_case  # noqa: E402
 
 
 def _ens(seed, shape, members, amp=0.3, base_amp=1.0):
@@ -71,6 +83,95 @@ MODELS = [
     ("histogram", 9),
     ("histogram", 16),
 ]
+
+
+KIND_CODE = {"uniform": 0, "epanechnikov": 1, "histogram": 2, "gaussian": 3}
+
+
+def _pack(cases):
+    """Flat per-distribution arrays: kind, a, b, bins and zero-padded weights."""
+    P = 1 + len(cases[0].neighbors)
+    maxb = 1
+    for c in cases:
+        for d in (c.center, *c.neighbors):
+            if getattr(d, "bin_weights", None) is not None:
+                maxb = max(maxb, d.bin_weights.size)
+    n = len(cases)
+    kind = np.zeros((n, P), np.int32)
+    a = np.zeros((n, P))
+    b = np.zeros((n, P))
+    bins = np.ones((n, P), np.int32)
+    w = np.zeros((n, P, maxb))
+    for i, c in enumerate(cases):
+        for p, d in enumerate((c.center, *c.neighbors)):
+            if isinstance(d, GaussianSampler):
+                kind[i, p], a[i, p], b[i, p] = 3, d.mean, d.stddev
+                continue
+            kind[i, p] = KIND_CODE[d.kind]
+            a[i, p], b[i, p] = d.support.lo, d.support.hi
+            if d.kind == "histogram":
+                bins[i, p] = d.bin_weights.size
+                w[i, p, :d.bin_weights.size] = d.bin_weights
+    return {"kind": kind, "a": a, "b": b, "bins": bins, "weights": w}
+
+
+def case_fixtures() -> dict:
+    """Per-case API goldens; groups by neighbourhood size."""
+    mixed = NeighborhoodCase(
+        epanechnikov(1.0, 0.9),
+        (histogram(0.2, 2.2, [0.3, 0.5, 0.2]), uniform(0.5, 2.5), epanechnikov(1.4, 1.0),
+         histogram(-0.2, 1.8, [0.25, 0.25, 0.5])))
+    kat = NeighborhoodCase(uniform(0.0, 2.0), (uniform(1.0, 3.0), uniform(0.5, 2.5),
+                                               uniform(1.5, 3.5), uniform(0.0, 2.0)))
+    disjoint = NeighborhoodCase(uniform(0.0, 1.0), tuple(uniform(2.0, 3.0) for _ in range(4)))
+    out = {}
+    for k in (4, 2):
+        cases, spec = [], []
+        per = 12 if k == 4 else 6
+        for model, bins in (("uniform", 5), ("epanechnikov", 5), ("histogram", 5), ("histogram", 3),
+                            ("histogram", 9), ("gaussian", 5)):
+            for s in range(per):
+                seed = 100 * len(spec) + s
+                cases.append(random_case(seed, model=model, neighborhood=k, bins=bins))
+                spec.append((seed, KIND_CODE[model], bins))
+        if k == 4:
+            cases += [mixed, kat, disjoint, disjoint.negate(), mixed.affine(2.5, -1.0),
+                      NeighborhoodCase(mixed.center, (mixed.neighbors[0], GaussianSampler(1.0, 0.4),
+                                                      mixed.neighbors[2], mixed.neighbors[3]))]
+        else:
+            cases += [NeighborhoodCase(uniform(0.0, 1.0), (uniform(2.0, 3.0), uniform(-3.0, -2.0))),
+                      NeighborhoodCase(mixed.center, mixed.neighbors[:2])]
+        pk = _pack(cases)
+        n = len(cases)
+        closed = np.full((n, 3), np.nan)
+        mc = np.zeros((n, 3))
+        semi = np.full((n, 3), np.nan)
+        comb = np.full((n, 3), np.nan)
+        pixels = (np.arange(n, dtype=np.uint64) * np.uint64(7919) + np.uint64(3))
+        for i, c in enumerate(cases):
+            dists = (c.center, *c.neighbors)
+            bounded = not any(isinstance(d, GaussianSampler) for d in dists)
+            if bounded:
+                closed[i] = tuple(closed_form_triple(c))
+            mc[i] = tuple(mc_all_patterns(c, 2001, seed=7, pixel=int(pixels[i])))
+            if bounded and all(d.kind == "histogram" for d in dists):
+                semi[i] = [semianalytical_prob(c, p, 700, seed=2, pixel=int(pixels[i]))
+                           for p in ("min", "max", "saddle")]
+                if max(d.bin_weights.size for d in dists) <= 5:
+                    comb[i] = tuple(combinatorial_triple(c))
+        for key, val in pk.items():
+            out[f"k{k}/{key}"] = val
+        out[f"k{k}/pixels"] = pixels
+        out[f"k{k}/random_spec"] = np.array(spec, dtype=np.int64)  # (seed, kind code, bins) of the first cases
+        out[f"k{k}/closed"] = closed
+        out[f"k{k}/mc"] = mc
+        out[f"k{k}/semi"] = semi
+        out[f"k{k}/comb"] = comb
+    out["mc/n"] = np.array(2001)
+    out["mc/seed"] = np.array(7)
+    out["semi/c"] = np.array(700)
+    out["semi/seed"] = np.array(2)
+    return out
 
 
 def main() -> None:
@@ -171,6 +272,7 @@ def main() -> None:
                 io_fx[f"heat/{ch}/{g}"] = np.frombuffer(open(os.path.join(tmp, "h.pgm"), "rb").read(), np.uint8)
         io_fx["prob/valid"] = prob.valid
     np.savez_compressed(os.path.join(HERE, "io.npz"), **io_fx)
+    np.savez_compressed(os.path.join(HERE, "cases.npz"), **case_fixtures())
 
     np.savez_compressed(os.path.join(HERE, "fit.npz"), **fit)
     np.savez_compressed(os.path.join(HERE, "closed.npz"), **closed)
@@ -178,7 +280,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **rng_fx)
     np.savez_compressed(os.path.join(HERE, "semi.npz"), **semi)
     np.savez_compressed(os.path.join(HERE, "comb.npz"), **comb)
-    for f in ("fit", "closed", "mc", "rng", "semi", "comb"):
+    for f in ("fit", "closed", "mc", "rng", "semi", "comb", "io", "cases"):
         print(f, os.path.getsize(os.path.join(HERE, f + ".npz")), "bytes")
 
 
