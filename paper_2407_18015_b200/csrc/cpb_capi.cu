@@ -316,7 +316,9 @@ int workspace_pool(cudaMemPool_t* out) {
 }
 
 }  // namespace
+}  // extern "C"
 
+namespace cpb {
 int workspace_alloc(void** p, size_t bytes, cudaStream_t st) {
   cudaMemPool_t pool;
   if (int rc = workspace_pool(&pool)) return rc;
@@ -328,6 +330,9 @@ int workspace_alloc(void** p, size_t bytes, cudaStream_t st) {
 void workspace_free(void* p, cudaStream_t st) {
   if (p) cudaFreeAsync(p, st);
 }
+}  // namespace cpb
+
+extern "C" {
 
 namespace {
 
