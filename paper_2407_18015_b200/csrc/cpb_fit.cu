@@ -42,6 +42,23 @@ struct FitArgs {
 
 CPB_D bool nonfinite(float v) { return (__float_as_uint(v) & 0x7f800000u) == 0x7f800000u; }
 
+// NaN-propagating min (PTX min.NaN): a running min over the members is NaN
+// iff some member is NaN, so one check after the loop replaces a per-member
+// test; +-Inf members show up in the min / max themselves.
+CPB_D float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+
+// 1 if x < t else 0, for finite x and a threshold t that is not +0.0 (callers
+// map +0 to -0): the sign of fl(x - t) is the sign of x - t (a nonzero
+// difference of two floats is at least the smallest subnormal, and no FTZ
+// here), and equal operands give +0 -- including x = +-0 against t = -0 --
+// so the count update "c += lt_bit(x, t)" is an FADD and a shift-add
+// (LEA.HI) per threshold.
+CPB_D uint32_t lt_bit(float x, float t) { return __float_as_uint(__fsub_rn(x, t)) >> 31; }
+
 // Block-level merge of the per-thread range into the global words.
 CPB_D void merge_range(float vmin, float vmax, bool bad, uint32_t* range) {
   uint32_t omin = float_to_ordered(vmin), omax = float_to_ordered(vmax);
@@ -219,19 +236,61 @@ constexpr int kThreshBins = 8;  // histogram bins counted with per-thread thresh
 // Smallest float v with floor(fl(fl(v - lo) * scale)) >= k -- the bin index of
 // fields.py:147 is monotone in v, so "bin >= k" is "v >= threshold_k" and the
 // per-member binning becomes h-1 float compares, bit-exact by construction.
-CPB_D float bin_threshold(int k, double lo, double scale) {
-  auto raw = [&](float v) { return floor(__dmul_rn(__dsub_rn((double)v, lo), scale)); };
-  float c = __double2float_rn(__dadd_rn(lo, __ddiv_rn((double)k, scale)));
+// Order-preserving map of finite floats to uint32 (-0 and +0 adjacent).
+CPB_D uint32_t fkey(float f) {
+  const uint32_t i = __float_as_uint(f);
+  return (i & 0x80000000u) ? ~i : (i | 0x80000000u);
+}
+CPB_D float fkey_inv(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+// The threshold is found on the float order itself: from the FP32 guess
+// (normally within an ulp: two evaluations) an exponential search brackets
+// the step of the monotone predicate raw(v) >= k inside [vlo, vhi] (the
+// pixel's min / max, where raw is 0 and >= h - 1 >= k), then bisection on
+// the keys pins it -- exact for any data, e.g. bins whose edge sits within
+// 1e-17 of zero, where the step is ~2^40 float ulps away from the guess.
+CPB_D float bin_threshold(int k, double lo, double scale, float guess, float vlo, float vhi) {
   const double kk = (double)k;
-  if (raw(c) >= kk) {
-    for (int it = 0; it < 64; ++it) {
-      const float d = nextafterf(c, -__int_as_float(0x7f800000));
-      if (raw(d) >= kk) c = d; else break;
+  auto pred = [&](uint32_t u) {
+    return floor(__dmul_rn(__dsub_rn((double)fkey_inv(u), lo), scale)) >= kk;
+  };
+  const uint32_t kmin = fkey(vlo), kmax = fkey(vhi);
+  uint32_t g = fkey(guess);
+  g = g < kmin ? kmin : (g > kmax ? kmax : g);
+  uint32_t lo_k, hi_k;  // pred(lo_k) false, pred(hi_k) true
+  if (pred(g)) {
+    hi_k = g;
+    uint32_t step = 1;
+    for (;;) {
+      const uint32_t c = (hi_k - kmin > step) ? hi_k - step : kmin;
+      if (!pred(c)) { lo_k = c; break; }
+      hi_k = c;
+      if (c == kmin) { lo_k = c; break; }  // unreachable: raw(vlo) = 0 < k
+      step <<= 1;
     }
   } else {
-    for (int it = 0; it < 64 && raw(c) < kk; ++it) c = nextafterf(c, __int_as_float(0x7f800000));
+    lo_k = g;
+    uint32_t step = 1;
+    for (;;) {
+      const uint32_t c = (kmax - lo_k > step) ? lo_k + step : kmax;
+      if (pred(c)) { hi_k = c; break; }
+      lo_k = c;
+      if (c == kmax) { hi_k = c; break; }  // unreachable: raw(vhi) >= h - 1 >= k
+      step <<= 1;
+    }
   }
-  return c;
+  while (hi_k - lo_k > 1) {
+    const uint32_t mid = lo_k + (hi_k - lo_k) / 2;
+    if (pred(mid)) hi_k = mid; else lo_k = mid;
+  }
+  return fkey_inv(hi_k);
+}
+
+CPB_D float bin_threshold(int k, double lo, double scale, float vlo, float vhi) {
+  return bin_threshold(k, lo, scale, __double2float_rn(__dadd_rn(lo, __ddiv_rn((double)k, scale))),
+                       vlo, vhi);
 }
 
 // NT: histogram bin count handled with NT-1 register thresholds (1..kThreshBins),
@@ -311,7 +370,7 @@ __global__ void __launch_bounds__(2 * kTmaTile) fit_tma_hist2_kernel(
       const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
       float thr[NT];
 #pragma unroll
-      for (int q = 1; q < NT; ++q) thr[q] = bin_threshold(q, dlo, scale);
+      for (int q = 1; q < NT; ++q) thr[q] = bin_threshold(q, dlo, scale, lo, hi);
 #pragma unroll 4
       for (int m = m0; m < m1; ++m) {
         const float x = col[m * kTmaTile];
@@ -393,11 +452,11 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
 #pragma unroll 8
       for (int m = 0; m < M; ++m) {
         const float x = col[m * kTmaTile];
-        bad |= nonfinite(x);
-        lo = fminf(lo, x);
+        lo = fmin_nan(lo, x);
         hi = fmaxf(hi, x);
         if (KIND == CPB_EPANECHNIKOV || KIND == CPB_GAUSSIAN) sum = __dadd_rn(sum, (double)x);
       }
+      bad |= nonfinite(lo) | nonfinite(hi);
       vmin = fminf(vmin, lo);
       vmax = fmaxf(vmax, hi);
       if (KIND == CPB_UNIFORM || KIND == CPB_HISTOGRAM) {
@@ -413,16 +472,22 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
         if (NT > 0) {
           // cumulative counts C_k = #{v >= thr_k}; bin b holds C_b - C_{b+1}
           float thr[NB];
+          const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)h);
 #pragma unroll
-          for (int q = 1; q < NB; ++q) thr[q] = hi > lo ? bin_threshold(q, dlo, scale) : 0.0f;
+          for (int q = 1; q < NB; ++q)
+            thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
+#pragma unroll
+          for (int q = 1; q < NB; ++q) thr[q] = thr[q] == 0.0f ? -0.0f : thr[q];  // +0 -> -0
 #pragma unroll
           for (int q = 0; q <= NB; ++q) c[q] = 0u;
 #pragma unroll 4
           for (int m = 0; m < M; ++m) {
             const float x = col[m * kTmaTile];
 #pragma unroll
-            for (int q = 1; q < NB; ++q) c[q] += (x >= thr[q]) ? 1u : 0u;
+            for (int q = 1; q < NB; ++q) c[q] += lt_bit(x, thr[q]);  // #{x < thr_q}
           }
+#pragma unroll
+          for (int q = 1; q < NB; ++q) c[q] = (uint32_t)M - c[q];  // C_q = #{x >= thr_q}
           c[0] = (uint32_t)M;
         } else {
           for (int b = 0; b < h; ++b) cnt[b * kTmaTile + tid] = 0u;

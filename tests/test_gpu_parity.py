@@ -463,3 +463,21 @@ def test_release_workspace_returns_cached_scratch():
     assert released.value > 0
     _lib.check(lib.cpb_release_workspace(ctypes.byref(released)))
     assert released.value == 0
+
+
+def test_fit_histogram_threshold_edges():
+    """Members at +-0, subnormals and exact bin edges: the exact threshold binning
+    (fields.py:146-152) including thresholds at zero."""
+    rng = np.random.default_rng(12)
+    tiny = np.float32(1e-45)
+    special = np.array([-0.0, 0.0, tiny, -tiny, -1.0, 1.0, 0.5, -0.5, 1e-38, -1e-38], dtype=np.float32)
+    H, W, M = 6, 40, 23
+    vals = rng.choice(special, size=(M, H, W)).astype(np.float32)
+    vals[0] = -1.0
+    vals[1] = 1.0
+    vals[:, 5, :20] = rng.uniform(-1, 1, (M, 20)).astype(np.float32)
+    for bins in (2, 3, 4, 5, 8, 9):
+        got = _fit(vals, "histogram", bins).params
+        ref = orc.fit(vals, "histogram", bins)
+        for k in ref:
+            assert np.array_equal(got[k], ref[k]), (bins, k)
