@@ -71,6 +71,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--serial", action="store_true", help="no fit/stencil overlap (one stream)")
+    p.add_argument("--fit", choices=("fused", "separate"), default="fused",
+                   help="fused: one cpb_fit_multi pass over the ensemble for all models per step; "
+                        "separate: one cpb_fit per model")
     p.add_argument("--fit-ctas", type=int, default=0,
                    help="persistent fit CTAs per SM while overlapping (0 = occupancy maximum)")
     p.add_argument("--profile", action="store_true", help="one short pass, for ncu")
@@ -186,36 +189,70 @@ def run_ours(args):
     est = cpb.EstimatorSpec()
     timer = KernelTimer()
     sums = {}
-    # one reusable halo-padded field per model; eps stays on the device, so the
-    # fits (HBM-bound, high-priority stream) run ahead and overlap the previous
-    # model's stencil (FP64-bound, low-priority stream)
-    fields = {k: D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models}
-    s_fit = torch.cuda.Stream(device=device, priority=-1)
-    s_cls = torch.cuda.Stream(device=device, priority=0)
-    fitted = {k: torch.cuda.Event() for k in models}
-    consumed = {k: torch.cuda.Event() for k in models}
     overlap = not args.serial
     if overlap and args.fit_ctas:
         from paper_2407_18015_b200 import _lib
 
         _lib.check(_lib.load().cpb_set_option(b"fit_ctas_per_sm", args.fit_ctas))
+    s_fit = torch.cuda.Stream(device=device, priority=-1)
+    s_cls = torch.cuda.Stream(device=device, priority=0)
+    fused = args.fit == "fused" and len(models) > 1
+    if fused:
+        # all models fitted in ONE pass over the ensemble (cpb_fit_multi); two
+        # sets of halo-padded planes alternate between steps, so the next
+        # step's fit (HBM-bound, high-priority stream) runs under this step's
+        # stencils (FP64-bound, low-priority stream)
+        nsets = 2 if overlap else 1
+        sets = [{k: D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models}
+                for _ in range(nsets)]
+        fitted = [torch.cuda.Event() for _ in range(nsets)]
+        consumed = [torch.cuda.Event() for _ in range(nsets)]
+        counter = [0]
 
-    def step():
-        for kind in models:
-            timer.kind = kind
+        def step():
+            b = counter[0] % nsets
+            counter[0] += 1
+            fs = sets[b]
+            timer.kind = "fused"
             with torch.cuda.stream(s_fit if overlap else torch.cuda.current_stream()):
                 if overlap:
-                    s_fit.wait_event(consumed[kind])  # last step's stencil is done with the planes
-                fields[kind].fit(ens, timer=timer)
-                fitted[kind].record()
+                    s_fit.wait_event(consumed[b])
+                D.fit_slab_fields([fs[k] for k in models], ens, timer=timer)
+                fitted[b].record()
             with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
                 if overlap:
-                    s_cls.wait_event(fitted[kind])
-                _, sums[kind] = D.classify_slab(fields[kind].dev, slab, est, out=out, sums=True,
-                                                timer=timer)
-                consumed[kind].record()
-        if overlap:
-            torch.cuda.current_stream().wait_stream(s_cls)
+                    s_cls.wait_event(fitted[b])
+                for kind in models:
+                    timer.kind = kind
+                    _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=out, sums=True,
+                                                    timer=timer)
+                consumed[b].record()
+            if overlap:
+                torch.cuda.current_stream().wait_stream(s_cls)
+    else:
+        # one reusable halo-padded field per model; eps stays on the device, so the
+        # fits (HBM-bound, high-priority stream) run ahead and overlap the previous
+        # model's stencil (FP64-bound, low-priority stream)
+        fields = {k: D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models}
+        fitted = {k: torch.cuda.Event() for k in models}
+        consumed = {k: torch.cuda.Event() for k in models}
+
+        def step():
+            for kind in models:
+                timer.kind = kind
+                with torch.cuda.stream(s_fit if overlap else torch.cuda.current_stream()):
+                    if overlap:
+                        s_fit.wait_event(consumed[kind])  # last step's stencil is done with the planes
+                    fields[kind].fit(ens, timer=timer)
+                    fitted[kind].record()
+                with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
+                    if overlap:
+                        s_cls.wait_event(fitted[kind])
+                    _, sums[kind] = D.classify_slab(fields[kind].dev, slab, est, out=out, sums=True,
+                                                    timer=timer)
+                    consumed[kind].record()
+            if overlap:
+                torch.cuda.current_stream().wait_stream(s_cls)
 
     def barrier():
         if world > 1:
@@ -256,7 +293,10 @@ def run_ours(args):
     kern = {}
     for (kind, what), times in per_kernel.items():
         t = statistics.mean(times)
-        if what == "fit":
+        if what == "fit" and kind == "fused":
+            nbytes = owned_px * (4 * M + sum(param_bytes(k, bins) for k in models))
+            name = "fit_tma_multi_kernel"
+        elif what == "fit":
             nbytes = owned_px * (4 * M + param_bytes(kind, bins))
             name = f"fit_tma_kernel<{kind}>"
         else:
@@ -283,7 +323,13 @@ def run_ours(args):
                          "note": "e2e algorithmic bytes 4M+24 per vertex per model"},
                 "kernels": {f"{k}/{w}": {"ms": round(r["ms"], 3), "GB/s": round(r["gbs"], 1)}
                             for (k, w), r in kern.items()}}
-    launches_per_step = sum(3 + (1 if k == "histogram" else 0) for k in models)
+    # our kernels per step: range init, fit(s), weight table (histogram),
+    # range->pair, pair->eps per field, one stencil per model
+    hist = 1 if "histogram" in models else 0
+    if fused:
+        launches_per_step = 1 + 1 + hist + 1 + 2 * len(models)
+    else:
+        launches_per_step = sum(5 + (1 if k == "histogram" else 0) for k in models)
 
     # ---- parity spot-check + CPU baseline (rank 0, N = 1)
     cpu = None
@@ -308,6 +354,8 @@ def run_ours(args):
                                    f"fit + min/max/saddle for {'+'.join(models)} (bins={bins})",
                        "height": H, "width": W, "members": M, "bins": bins, "models": models,
                        "vertices_per_model": verts, "parallelism": f"row-slab x{world}",
+                       "fit": "one fused pass over the ensemble for all models" if fused else
+                              "one pass per model",
                        "l2": "inputs (68.7 GB ensemble) larger than L2; no flush needed"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps,

@@ -7,6 +7,7 @@
  * (citations are /root/reference/pkg/src/critprob/<file>:<line>):
  *
  *   cpb_fit              UncertainField.from_ensemble      fields.py:125-158
+ *   cpb_fit_multi        from_ensemble of several models over one stack (one HBM pass)
  *   cpb_from_scalar      UncertainField.from_scalar        fields.py:160-178
  *   cpb_epsilon          default_epsilon                   distributions.py:30-36
  *   cpb_classify_closed  classify_field, closed form       engine.py:716-787 (+ _closed_chunk 594-629)
@@ -155,6 +156,15 @@ int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d
  * (distributions.py:30-36), for cpb_field.eps_device. */
 int cpb_range_to_pair(const uint32_t* d_range, double* d_pair, void* stream);
 int cpb_pair_to_eps(const double* d_pair, double* d_eps, void* stream);
+
+/* Fit several models of ONE ensemble in a single pass over it (the reference
+ * workflow: one EnsembleStack, from_ensemble per model).  All fields share
+ * height, width and members; each gets exactly the planes cpb_fit would write
+ * (bit-identical), and d_range receives the shared data range.  At most one
+ * field per kind is fused (histograms with <= 8 bins); other sets are fitted
+ * one after another. */
+int cpb_fit_multi(const float* d_ens, int64_t member_stride, cpb_field* const* fields,
+                  int32_t n_fields, uint32_t* d_range, int32_t accumulate, void* stream);
 
 /* Synchronously read back a d_range written by cpb_fit; returns
  * CPB_ENONFINITE if any value was NaN/Inf. */

@@ -37,6 +37,8 @@ int launch_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end,
 int launch_heatmap(const double* p, const uint8_t* valid, int64_t n, double gamma, uint8_t* out,
                    cudaStream_t st);
 int launch_eps_sensitive_rows(const cpb_field* f, double eps, uint8_t* sens, cudaStream_t st);
+int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, int n, uint32_t* range,
+                     bool accumulate, cudaStream_t st);
 int launch_cases_closed(const cpb_case_batch* b, double* out, cudaStream_t st);
 int launch_cases_mc(const cpb_case_batch* b, uint64_t seed, const uint64_t* pixels, int64_t n,
                     unsigned long long* counts, double* out, cudaStream_t st);
@@ -143,6 +145,46 @@ int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d
   if (member_stride < f->height * f->width) { set_error("member_stride smaller than a member plane"); return CPB_EINVAL; }
   if (!d_ens || !d_range) { set_error("NULL ensemble or range pointer"); return CPB_EINVAL; }
   return launch_fit(d_ens, member_stride, f, d_range, accumulate != 0, (cudaStream_t)stream);
+}
+
+int cpb_fit_multi(const float* d_ens, int64_t member_stride, cpb_field* const* fields,
+                  int32_t n_fields, uint32_t* d_range, int32_t accumulate, void* stream) {
+  if (!fields || n_fields < 1 || n_fields > 16) { set_error("1..16 fields expected"); return CPB_EINVAL; }
+  for (int i = 0; i < n_fields; ++i) {
+    cpb_field* f = fields[i];
+    if (!f) { set_error("NULL field"); return CPB_EINVAL; }
+    if (f->height != fields[0]->height || f->width != fields[0]->width ||
+        f->members != fields[0]->members) {
+      set_error("fields of one fused fit must share height, width and members");
+      return CPB_EINVAL;
+    }
+  }
+  // validation (and, when the fused kernel does not cover the set, the fits
+  // themselves) through the single-model entry point
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < n_fields; ++i) {
+    int s = check_field(fields[i], false);
+    if (s) return s;
+    cpb_field* f = fields[i];
+    if (f->members < 1) { set_error("ensemble needs at least one member"); return CPB_EINVAL; }
+    if (f->members < 2 && (f->kind == CPB_EPANECHNIKOV || f->kind == CPB_GAUSSIAN)) {
+      set_error("%s fit needs at least two members", f->kind == CPB_EPANECHNIKOV ? "epanechnikov" : "gaussian");
+      return CPB_EINVAL;
+    }
+    if (f->kind == CPB_HISTOGRAM && f->members > 65535) {
+      set_error("histogram fit supports at most 65535 members");
+      return CPB_EINVAL;
+    }
+  }
+  if (member_stride < fields[0]->height * fields[0]->width) { set_error("member_stride smaller than a member plane"); return CPB_EINVAL; }
+  if (!d_ens || !d_range) { set_error("NULL ensemble or range pointer"); return CPB_EINVAL; }
+  const int rc = n_fields > 1 ? launch_fit_multi(d_ens, member_stride, fields, n_fields, d_range, accumulate != 0, st) : 1;
+  if (rc != 1) return rc;
+  for (int i = 0; i < n_fields; ++i) {
+    int s = launch_fit(d_ens, member_stride, fields[i], d_range, accumulate != 0 || i > 0, st);
+    if (s) return s;
+  }
+  return CPB_OK;
 }
 
 int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* stream) {

@@ -549,6 +549,155 @@ __global__ void pair_eps_kernel(const double* pair, double* eps) {
   *eps = e != e ? e : (e > 1e-12 ? e : 1e-12);
 }
 
+// ---------------------------------------------------------------------------
+// Several models over ONE read of the ensemble (the reference workflow fits
+// one EnsembleStack with every model, fields.py:125-158 per model): each
+// TMA-staged tile feeds the shared min / max pass (uniform and histogram
+// bounds are the same numbers), the histogram threshold binning and the
+// Epanechnikov / Gaussian moment passes, so HBM sees the ensemble once
+// instead of once per model.  Same arithmetic as the single-model kernels,
+// so every plane is bit-identical to a separate cpb_fit.
+struct MultiArgs {
+  int64_t npix, wstride;
+  int members, bins;
+  float* lo[2];       // uniform, histogram bounds (either may be NULL)
+  float* hi[2];
+  double* mean[2];    // epanechnikov, gaussian moments (either may be NULL)
+  double* spread[2];
+  void* counts;       // histogram bin counts (bins, npix)
+  int wmode;
+  uint32_t* range;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
+    const __grid_constant__ CUtensorMap map, MultiArgs a, int stages, int mbox, int nbox,
+    int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int M = a.members;
+  const int rows = mbox * nbox;
+  const int tid = threadIdx.x;
+  float* buf = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * rows * kTmaTile * 4);
+  if (tid == 0) {
+    prefetch_tensormap(&map);
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const uint32_t tile_bytes = (uint32_t)rows * kTmaTile * 4u;
+  auto issue = [&](int64_t tile, int s) {
+    mbar_arrive_expect_tx(&full[s], tile_bytes);
+    float* dst = buf + (size_t)s * rows * kTmaTile;
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(dst + (size_t)b * mbox * kTmaTile, &map, (int)(tile * kTmaTile), b * mbox, &full[s], pol);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < stages; ++k) {
+      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+      if (t < ntiles) issue(t, k);
+    }
+  }
+  const bool moments = a.mean[0] || a.mean[1];
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % stages;
+    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+    const float* col = buf + (size_t)s * rows * kTmaTile + tid;
+    const int64_t p = t * kTmaTile + tid;
+    if (p < a.npix) {
+      float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+      double sum = 0.0;
+      if (moments) {
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const float x = col[m * kTmaTile];
+          lo = fmin_nan(lo, x);
+          hi = fmaxf(hi, x);
+          sum = __dadd_rn(sum, (double)x);
+        }
+      } else {
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const float x = col[m * kTmaTile];
+          lo = fmin_nan(lo, x);
+          hi = fmaxf(hi, x);
+        }
+      }
+      bad |= nonfinite(lo) | nonfinite(hi);
+      vmin = fminf(vmin, lo);
+      vmax = fmaxf(vmax, hi);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (a.lo[i]) {
+          a.lo[i][p] = lo;
+          a.hi[i][p] = hi;
+        }
+      }
+      if (NT > 0 && a.counts) {
+        const int h = a.bins;
+        const double dlo = (double)lo;
+        const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
+        constexpr int NB = NT > 0 ? NT : 1;
+        uint32_t c[NB + 1];
+        float thr[NB];
+        const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)h);
+#pragma unroll
+        for (int q = 1; q < NT; ++q) {
+          thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
+          thr[q] = thr[q] == 0.0f ? -0.0f : thr[q];
+        }
+#pragma unroll
+        for (int q = 0; q <= NT; ++q) c[q] = 0u;
+#pragma unroll 4
+        for (int m = 0; m < M; ++m) {
+          const float x = col[m * kTmaTile];
+#pragma unroll
+          for (int q = 1; q < NT; ++q) c[q] += lt_bit(x, thr[q]);
+        }
+#pragma unroll
+        for (int q = 1; q < NT; ++q) c[q] = (uint32_t)M - c[q];
+        c[0] = (uint32_t)M;
+        const bool flat = !(hi > lo);
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+          const uint32_t v = flat ? 0u : (b + 1 < NT ? c[b] - c[b + 1] : c[b]);
+          if (a.wmode == CPB_WEIGHTS_U8)
+            static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
+          else
+            static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
+        }
+      }
+      if (moments) {
+        const double mean = __ddiv_rn(sum, (double)M);
+        double sq = 0.0;
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const double d = __dsub_rn((double)col[m * kTmaTile], mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+        const double sd = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (a.mean[i]) {
+            a.mean[i][p] = mean;
+            a.spread[i][p] = sd;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)stages * gridDim.x;
+      if (tn < ntiles) issue(tn, s);
+    }
+  }
+  merge_range(vmin, vmax, bad, a.range);
+}
+
 __global__ void range_init_kernel(uint32_t* range) {
   range[0] = 0xffffffffu;
   range[1] = 0u;
@@ -915,4 +1064,106 @@ int launch_eps_sensitive_rows(const cpb_field* fld, double eps, uint8_t* sens, c
   CPB_CHECK_LAUNCH("eps sensitivity kernel");
   return CPB_OK;
 }
+
+// Fused fit of several models (see fit_tma_multi_kernel).  Returns 1 (nothing
+// launched) when the combination or layout is not covered -- the caller then
+// fits the fields one by one.
+int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, int n,
+                     uint32_t* range, bool accumulate, cudaStream_t st) {
+  cpb_field* slot[4] = {nullptr, nullptr, nullptr, nullptr};  // uniform, histogram, epan, gaussian
+  for (int i = 0; i < n; ++i) {
+    const int k = fs[i]->kind;
+    const int q = k == CPB_UNIFORM ? 0 : k == CPB_HISTOGRAM ? 1 : k == CPB_EPANECHNIKOV ? 2 : 3;
+    if (slot[q]) return 1;
+    slot[q] = fs[i];
+  }
+  const cpb_field* f0 = fs[0];
+  if (slot[1] && slot[1]->bins > kThreshBins) return 1;
+  const int64_t npix = f0->height * f0->width;
+  const int mbox = std::min(f0->members, 256);
+  const int nbox = (f0->members + mbox - 1) / mbox;
+  const size_t tile_bytes = (size_t)mbox * nbox * kTmaTile * 4;
+  if (!((mstride % 4 == 0) && ((reinterpret_cast<uintptr_t>(ens) & 15) == 0) &&
+        tile_bytes * 2 + 64 <= 200 * 1024))
+    return 1;
+  MultiArgs a = {};
+  a.npix = npix;
+  a.members = f0->members;
+  a.wmode = f0->members <= 255 ? CPB_WEIGHTS_U8 : CPB_WEIGHTS_U16;
+  a.range = range;
+  for (int i = 0; i < 2; ++i) {
+    if (slot[i]) {
+      a.lo[i] = static_cast<float*>(slot[i]->lo);
+      a.hi[i] = static_cast<float*>(slot[i]->hi);
+      slot[i]->bounds = CPB_BOUNDS_F32_FITTED;
+      slot[i]->weights_mode = CPB_WEIGHTS_F64;
+    }
+    if (slot[2 + i]) {
+      a.mean[i] = slot[2 + i]->mean;
+      a.spread[i] = slot[2 + i]->spread;
+      slot[2 + i]->bounds = CPB_BOUNDS_F32_FITTED;
+      slot[2 + i]->weights_mode = CPB_WEIGHTS_F64;
+    }
+  }
+  int nt = 0;
+  if (slot[1]) {
+    nt = slot[1]->bins;
+    a.bins = nt;
+    a.counts = slot[1]->weights;
+    a.wstride = slot[1]->plane_stride > 0 ? slot[1]->plane_stride : npix;
+    slot[1]->weights_mode = a.wmode;
+  }
+  if (!accumulate) {
+    range_init_kernel<<<1, 1, 0, st>>>(range);
+    CPB_CHECK_LAUNCH("range init");
+  }
+  if (npix == 0) return CPB_OK;
+  if (slot[1]) {
+    weight_table_kernel<<<grid_for(a.members + 1, 256), 256, 0, st>>>(slot[1]->weight_table, a.members);
+    CPB_CHECK_LAUNCH("weight table");
+  }
+  static const int stage_kb = [] { const char* e = getenv("CPB_FIT_STAGE_KB"); return e ? atoi(e) : 64; }();
+  const int stages = (int)std::min<size_t>(8, std::max<size_t>(2, ((size_t)stage_kb * 1024) / tile_bytes));
+  const size_t smem = stages * tile_bytes + stages * 8;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t max_chunk = (int64_t)1 << 30;
+  for (int64_t p0 = 0; p0 < npix; p0 += max_chunk) {
+    MultiArgs c = a;
+    const int64_t cn = std::min(max_chunk, npix - p0);
+    c.npix = cn;
+    for (int i = 0; i < 2; ++i) {
+      if (c.lo[i]) { c.lo[i] += p0; c.hi[i] += p0; }
+      if (c.mean[i]) { c.mean[i] += p0; c.spread[i] += p0; }
+    }
+    if (c.counts) c.counts = static_cast<char*>(c.counts) + p0 * (a.wmode == CPB_WEIGHTS_U8 ? 1 : 2);
+    CUtensorMap map;
+    if (!encode_tensor_map_2d_f32(&map, ens + p0, (uint64_t)cn, (uint64_t)a.members,
+                                  (uint64_t)mstride * 4, kTmaTile, (uint32_t)mbox)) {
+      set_error("cuTensorMapEncodeTiled failed");
+      return CPB_ECUDA;
+    }
+    const int64_t ntiles = (cn + kTmaTile - 1) / kTmaTile;
+#define CPB_MULTI(NTV)                                                                         \
+  case NTV: {                                                                                  \
+    auto kern = fit_tma_multi_kernel<NTV>;                                                     \
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    int per_sm = 1;                                                                            \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaTile, smem);              \
+    if (g_fit_ctas_per_sm > 0) per_sm = std::min(per_sm, g_fit_ctas_per_sm);                  \
+    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));        \
+    kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);          \
+  } break;
+    switch (nt) {
+      CPB_MULTI(0) CPB_MULTI(1) CPB_MULTI(2) CPB_MULTI(3) CPB_MULTI(4)
+      CPB_MULTI(5) CPB_MULTI(6) CPB_MULTI(7) CPB_MULTI(8)
+      default: return 1;
+    }
+#undef CPB_MULTI
+    CPB_CHECK_LAUNCH("fused multi-model fit kernel");
+  }
+  return CPB_OK;
+}
+
 }  // namespace cpb

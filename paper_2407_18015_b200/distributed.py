@@ -229,6 +229,47 @@ class SlabField:
         return self.dev
 
 
+def fit_slab_fields(fields, ens_slab, group=None, timer=None):
+    """Fit several SlabFields of one slab in a single pass over the ensemble
+    (cpb_fit_multi); then the shared global eps and each field's halo exchange."""
+    import ctypes
+
+    from . import _lib
+
+    lib = _lib.load()
+    s = _lib.stream_ptr()
+    f0 = fields[0]
+    rng = f0.dev.tensors["range"].data_ptr()
+    views = (ctypes.POINTER(_lib.CpbField) * len(fields))(*[ctypes.pointer(f.view) for f in fields])
+    if timer:
+        timer("fit", True)
+    _lib.check(lib.cpb_fit_multi(ens_slab.data_ptr(), f0.slab.owned * f0.width, views, len(fields),
+                                 rng, 0, s))
+    if timer:
+        timer("fit", False)
+    for f in fields:
+        st = f.dev.struct
+        st.bounds, st.weights_mode, st.plane_stride = f.view.bounds, f.view.weights_mode, 0
+    if all(f.device_eps for f in fields):
+        _lib.check(lib.cpb_range_to_pair(rng, f0.pair.data_ptr(), s))
+        _, world = _group_world(group)
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(f0.pair, op=dist.ReduceOp.MAX, group=group)
+        for f in fields:
+            _lib.check(lib.cpb_pair_to_eps(f0.pair.data_ptr(), f.eps_t.data_ptr(), s))
+    else:
+        gmin, gmax = ctypes.c_double(), ctypes.c_double()
+        _lib.check(lib.cpb_read_range(rng, ctypes.byref(gmin), ctypes.byref(gmax), s))
+        gmin, gmax = allreduce_range(gmin.value, gmax.value, ens_slab.device, group)
+        for f in fields:
+            f.dev.eps = lib.cpb_epsilon(gmin, gmax)
+    for f in fields:
+        exchange_halo_rows(_plane_views(f.dev), f.slab, group)
+    return [f.dev for f in fields]
+
+
 def fit_slab(ens_slab, model, slab: Slab, width: int, group=None, timer=None):
     """Fit a rank's owned rows into halo-padded planes; global eps; halo exchange.
 

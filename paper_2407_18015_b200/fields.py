@@ -309,6 +309,19 @@ class UncertainField:
         return cls(model, _device_field=dev)
 
     @classmethod
+    def from_ensemble_models(cls, stack: EnsembleStack, models) -> list:
+        """``[from_ensemble(stack, m) for m in models]`` in one pass over the
+        ensemble (cpb_fit_multi): the reference workflow of fitting one stack
+        with several models, with the stack read from HBM once."""
+        models = list(models)
+        vals = stack.device_values()
+        M = int(vals.shape[0])
+        for model in models:
+            if M < 2 and model.kind in ("epanechnikov", "gaussian"):
+                raise ValueError(f"{model.kind} fit needs at least two members")
+        return [cls(m, _device_field=d) for m, d in zip(models, fit_device_models(vals, models))]
+
+    @classmethod
     def from_scalar(cls, values, error_bound: float) -> "UncertainField":
         """Uniform field from a plain raster with a +/- error_bound / 2 band (fields.py:160-178)."""
         import torch
@@ -367,6 +380,31 @@ def fit_device(vals, model: ModelSpec, *, row0: int = 0, global_width: int | Non
         range_out[:] = [gmin.value, gmax.value]
     dev.eps = lib.cpb_epsilon(gmin.value, gmax.value) if eps is None else eps
     return dev
+
+
+def fit_device_models(vals, models, *, row0: int = 0, global_width: int | None = None,
+                      eps: float | None = None, range_out: list | None = None) -> list:
+    """cpb_fit_multi over a (M, H, W) float32 CUDA tensor: one DeviceField per model."""
+    M, H, W = (int(s) for s in vals.shape)
+    lib = _lib.load()
+    devs = []
+    for model in models:
+        dev = DeviceField(model.kind, model.bins, M, H, W, row0=row0, global_width=global_width,
+                          k=model.k, device=vals.device)
+        dev.allocate_fitted()
+        devs.append(dev)
+    s = _lib.stream_ptr()
+    rng = devs[0].tensors["range"].data_ptr()
+    arr = (ctypes.POINTER(_lib.CpbField) * len(devs))(*[ctypes.pointer(d.struct) for d in devs])
+    _lib.check(lib.cpb_fit_multi(vals.data_ptr(), H * W, arr, len(devs), rng, 0, s))
+    gmin, gmax = ctypes.c_double(), ctypes.c_double()
+    _lib.check(lib.cpb_read_range(rng, ctypes.byref(gmin), ctypes.byref(gmax), s))
+    if range_out is not None:
+        range_out[:] = [gmin.value, gmax.value]
+    e = lib.cpb_epsilon(gmin.value, gmax.value) if eps is None else eps
+    for dev in devs:
+        dev.eps = e
+    return devs
 
 
 @dataclass

@@ -481,3 +481,25 @@ def test_fit_histogram_threshold_edges():
         ref = orc.fit(vals, "histogram", bins)
         for k in ref:
             assert np.array_equal(got[k], ref[k]), (bins, k)
+
+
+def test_fit_multi_matches_separate_fits():
+    """cpb_fit_multi (one pass, all models) writes exactly the planes of separate fits."""
+    rng = np.random.default_rng(21)
+    vals = (rng.uniform(-1, 1, (37, 53)) + rng.uniform(-0.3, 0.3, (17, 37, 53))).astype(np.float32)
+    vals[:, 4, 4] = 0.125  # degenerate pixel
+    stack = cpb.EnsembleStack(vals)
+    for models in ([cpb.ModelSpec("uniform"), cpb.ModelSpec("epanechnikov"), cpb.ModelSpec("histogram", bins=5)],
+                   [cpb.ModelSpec("histogram", bins=8), cpb.ModelSpec("gaussian")],
+                   [cpb.ModelSpec("histogram", bins=12), cpb.ModelSpec("uniform")],   # > 8 bins: separate
+                   [cpb.ModelSpec("histogram", bins=3), cpb.ModelSpec("histogram", bins=4)]):
+        fused = cpb.UncertainField.from_ensemble_models(stack, models)
+        for m, f in zip(models, fused):
+            ref = orc.fit(vals, m.kind, m.bins)
+            got = f.params
+            for k in ref:
+                assert np.array_equal(got[k], ref[k]), (m, k)
+            p = cpb.classify_field(f)
+            q = cpb.classify_field(cpb.UncertainField.from_ensemble(stack, m)) if m.kind != "gaussian" else p
+            if m.kind != "gaussian":
+                assert np.array_equal(p.p_min, q.p_min) and np.array_equal(p.p_saddle, q.p_saddle)
