@@ -637,34 +637,57 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
           a.hi[i][p] = hi;
         }
       }
-      if (NT > 0 && a.counts) {
-        const int h = a.bins;
-        const double dlo = (double)lo;
-        const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
-        constexpr int NB = NT > 0 ? NT : 1;
-        uint32_t c[NB + 1];
-        float thr[NB];
-        const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)h);
+      // second pass: histogram binning and the squared deviations share each
+      // member load
+      const bool hist = NT > 0 && a.counts != nullptr;
+      constexpr int NB = NT > 0 ? NT : 1;
+      uint32_t c[NB + 1];
+      float thr[NB];
 #pragma unroll
-        for (int q = 1; q < NT; ++q) {
+      for (int q = 0; q <= NB; ++q) c[q] = 0u;
+      if (hist) {
+        const double dlo = (double)lo;
+        const double scale = __ddiv_rn((double)a.bins, __dsub_rn((double)hi, dlo));
+        const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)a.bins);
+#pragma unroll
+        for (int q = 1; q < NB; ++q) {
           thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
           thr[q] = thr[q] == 0.0f ? -0.0f : thr[q];
         }
-#pragma unroll
-        for (int q = 0; q <= NT; ++q) c[q] = 0u;
+      }
+      const double mean = moments ? __ddiv_rn(sum, (double)M) : 0.0;
+      double sq = 0.0;
+      if (hist && moments) {
 #pragma unroll 4
         for (int m = 0; m < M; ++m) {
           const float x = col[m * kTmaTile];
 #pragma unroll
-          for (int q = 1; q < NT; ++q) c[q] += lt_bit(x, thr[q]);
+          for (int q = 1; q < NB; ++q) c[q] += lt_bit(x, thr[q]);
+          const double d = __dsub_rn((double)x, mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
         }
+      } else if (hist) {
+#pragma unroll 4
+        for (int m = 0; m < M; ++m) {
+          const float x = col[m * kTmaTile];
 #pragma unroll
-        for (int q = 1; q < NT; ++q) c[q] = (uint32_t)M - c[q];
+          for (int q = 1; q < NB; ++q) c[q] += lt_bit(x, thr[q]);
+        }
+      } else if (moments) {
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const double d = __dsub_rn((double)col[m * kTmaTile], mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+      }
+      if (hist) {
+#pragma unroll
+        for (int q = 1; q < NB; ++q) c[q] = (uint32_t)M - c[q];
         c[0] = (uint32_t)M;
         const bool flat = !(hi > lo);
 #pragma unroll
-        for (int b = 0; b < NT; ++b) {
-          const uint32_t v = flat ? 0u : (b + 1 < NT ? c[b] - c[b + 1] : c[b]);
+        for (int b = 0; b < NB; ++b) {
+          const uint32_t v = flat ? 0u : (b + 1 < NB ? c[b] - c[b + 1] : c[b]);
           if (a.wmode == CPB_WEIGHTS_U8)
             static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
           else
@@ -672,13 +695,6 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
         }
       }
       if (moments) {
-        const double mean = __ddiv_rn(sum, (double)M);
-        double sq = 0.0;
-#pragma unroll 8
-        for (int m = 0; m < M; ++m) {
-          const double d = __dsub_rn((double)col[m * kTmaTile], mean);
-          sq = __dadd_rn(sq, __dmul_rn(d, d));
-        }
         const double sd = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
