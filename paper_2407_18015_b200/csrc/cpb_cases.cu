@@ -273,51 +273,78 @@ CPB_D double draw_any(const PosTab& t, double u, double u2) {
   }
 }
 
+template <int KIND>
+CPB_D double draw_k(const PosTab& t, double u, double u2) {
+  if (KIND < 0) return draw_any(t, u, u2);
+  return draw<KIND < 0 ? 0 : KIND>(t.s, u, u2, KIND == CPB_HISTOGRAM ? t.h : 1);
+}
+
+// The sample loop for P positions (compile time) whose kinds are all KIND
+// (or mixed, KIND = -1): everything per position lives in registers.
+template <int P, int KIND>
+CPB_D void mc_loop(const PosTab (&t)[P], const uint64_t (&key)[2 * P], int64_t base, int64_t n,
+                   uint32_t& cmin, uint32_t& cmax, uint32_t& csad) {
+#pragma unroll 2
+  for (int r = 0; r < kMcPerThread; ++r) {
+    const int64_t i = base + (int64_t)r * kMcThreads + threadIdx.x;
+    if (i >= n) break;
+    double x[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const double u = stream_u01(key[2 * p], (uint64_t)i);
+      const bool gauss = KIND == CPB_GAUSSIAN || (KIND < 0 && t[p].kind == CPB_GAUSSIAN);
+      const double u2 = gauss ? stream_u01(key[2 * p + 1], (uint64_t)i) : 0.0;
+      x[p] = draw_k<KIND>(t[p], u, u2);
+    }
+    // strict comparisons, ties count against every pattern (_pattern_stats, engine.py:195-222)
+    if (P == 3) {
+      const bool la = x[0] < x[1], lb = x[0] < x[2 % P], ga = x[0] > x[1], gb = x[0] > x[2 % P];
+      cmin += la & lb;
+      cmax += ga & gb;
+      csad += (la & gb) | (ga & lb);
+    } else {
+      const bool lE = x[0] < x[1], lN = x[0] < x[2 % P], lW = x[0] < x[3 % P], lS = x[0] < x[4 % P];
+      const bool gE = x[0] > x[1], gN = x[0] > x[2 % P], gW = x[0] > x[3 % P], gS = x[0] > x[4 % P];
+      cmin += lE & lN & lW & lS;
+      cmax += gE & gN & gW & gS;
+      csad += (lE & gN & lW & gS) | (gE & lN & gW & lS);
+    }
+  }
+}
+
+template <int K>
 __global__ void __launch_bounds__(kMcThreads) cases_mc_kernel(Batch B, uint64_t seed,
                                                               const uint64_t* pixels, int64_t n,
                                                               int64_t chunks,
                                                               unsigned long long* counts) {
+  constexpr int P = K + 1;
   extern __shared__ double s_tab[];
   __shared__ PosTab pt[kMaxPos];
   __shared__ uint32_t red[3][kMcThreads / 32];
   const int64_t c = (int64_t)blockIdx.x / chunks;
   const int64_t chunk = (int64_t)blockIdx.x % chunks;
-  const int P = B.k + 1;
   const int tabw = 2 * B.maxb + 1;
   load_samplers(B, c, pt, s_tab, tabw, true);
   const uint64_t px = pixels ? pixels[c] : (uint64_t)c;
   const uint64_t pk = pixel_key(seed, px);
-  PosTab t[kMaxPos];
-  uint64_t key[2 * kMaxPos];
+  PosTab t[P];
+  uint64_t key[2 * P];
+  bool same = true;
+#pragma unroll
   for (int p = 0; p < P; ++p) {
     t[p] = pt[p];
     key[2 * p] = plane_key(pk, (uint64_t)t[p].plane);
     key[2 * p + 1] = plane_key(pk, (uint64_t)t[p].plane + 1);
+    same &= t[p].kind == t[0].kind;
   }
   uint32_t cmin = 0, cmax = 0, csad = 0;
   const int64_t base = chunk * (int64_t)kMcThreads * kMcPerThread;
-  for (int r = 0; r < kMcPerThread; ++r) {
-    const int64_t i = base + (int64_t)r * kMcThreads + threadIdx.x;
-    if (i >= n) break;
-    double x[kMaxPos];
-    for (int p = 0; p < P; ++p) {
-      const double u = stream_u01(key[2 * p], (uint64_t)i);
-      const double u2 = t[p].kind == CPB_GAUSSIAN ? stream_u01(key[2 * p + 1], (uint64_t)i) : 0.0;
-      x[p] = draw_any(t[p], u, u2);
-    }
-    // strict comparisons, ties count against every pattern (_pattern_stats, engine.py:195-222)
-    if (P == 3) {
-      const bool la = x[0] < x[1], lb = x[0] < x[2], ga = x[0] > x[1], gb = x[0] > x[2];
-      cmin += la & lb;
-      cmax += ga & gb;
-      csad += (la & gb) | (ga & lb);
-    } else {
-      const bool lE = x[0] < x[1], lN = x[0] < x[2], lW = x[0] < x[3], lS = x[0] < x[4];
-      const bool gE = x[0] > x[1], gN = x[0] > x[2], gW = x[0] > x[3], gS = x[0] > x[4];
-      cmin += lE & lN & lW & lS;
-      cmax += gE & gN & gW & gS;
-      csad += (lE & gN & lW & gS) | (gE & lN & gW & lS);
-    }
+  switch (same ? t[0].kind : -1) {
+    case CPB_UNIFORM: mc_loop<P, CPB_UNIFORM>(t, key, base, n, cmin, cmax, csad); break;
+    case CPB_EPANECHNIKOV: mc_loop<P, CPB_EPANECHNIKOV>(t, key, base, n, cmin, cmax, csad); break;
+    case CPB_HISTOGRAM: mc_loop<P, CPB_HISTOGRAM>(t, key, base, n, cmin, cmax, csad); break;
+    case CPB_GAUSSIAN: mc_loop<P, CPB_GAUSSIAN>(t, key, base, n, cmin, cmax, csad); break;
+    default: mc_loop<P, -1>(t, key, base, n, cmin, cmax, csad); break;
   }
   cmin = __reduce_add_sync(0xffffffffu, cmin);
   cmax = __reduce_add_sync(0xffffffffu, cmax);
@@ -330,9 +357,9 @@ __global__ void __launch_bounds__(kMcThreads) cases_mc_kernel(Batch B, uint64_t 
   }
   __syncthreads();
   if (threadIdx.x < 3) {
-    unsigned long long s = 0;
-    for (int q = 0; q < kMcThreads / 32; ++q) s += red[threadIdx.x][q];
-    if (s) atomicAdd(counts + 3 * c + threadIdx.x, s);
+    unsigned long long sum = 0;
+    for (int q = 0; q < kMcThreads / 32; ++q) sum += red[threadIdx.x][q];
+    if (sum) atomicAdd(counts + 3 * c + threadIdx.x, sum);
   }
 }
 
@@ -534,9 +561,10 @@ int launch_cases_mc(const cpb_case_batch* b, uint64_t seed, const uint64_t* pixe
   cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)B.n * 3 * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return cuda_status(e, "memset counts");
   const size_t smem = (size_t)kMaxPos * (2 * B.maxb + 1) * sizeof(double);
+  auto kern = B.k == 2 ? cases_mc_kernel<2> : cases_mc_kernel<4>;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(cases_mc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cases_mc_kernel<<<(unsigned)(chunks * B.n), kMcThreads, smem, st>>>(B, seed, pixels, n, chunks, cnt);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  kern<<<(unsigned)(chunks * B.n), kMcThreads, smem, st>>>(B, seed, pixels, n, chunks, cnt);
   CPB_CHECK_LAUNCH("per-case Monte Carlo kernel");
   cases_finish_kernel<<<(unsigned)((3 * B.n + 255) / 256), 256, 0, st>>>(cnt, B.n, n, out);
   CPB_CHECK_LAUNCH("per-case Monte Carlo finish");
