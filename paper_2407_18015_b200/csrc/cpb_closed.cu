@@ -76,6 +76,37 @@ CPB_D void integrands(const double* F, double g[4]) {
   g[3] = snss * fefw;
 }
 
+// GL3 sums of the four integrands on one piece from the neighbour CDFs at
+// the piece midpoint (Fm) and their slopes times the node offset (d): with
+// F = Fm +- d at the nodes mid +- tau, each pair product X*Y is Pe +- Po
+// (Pe = x0 y0 + dx dy, Po = x0 dy + y0 dx), so an integrand P*Q summed over
+// the two symmetric nodes is 2 (Pe Qe + Po Qo) and the midpoint value is
+// x0 y0 * ... : 58 FP64 operations instead of 69 for three separate nodes.
+// s[q] = w1 g_q(mid) + w0 (g_q(mid - tau) + g_q(mid + tau)).
+CPB_D void gl3_sym_sums(const double* Fm, const double* d, double s[4]) {
+  struct Pair { double p0, pe, po; };
+  auto pair = [](double x0, double dx, double y0, double dy) {
+    Pair r;
+    r.p0 = x0 * y0;
+    r.pe = fma(dx, dy, r.p0);
+    r.po = fma(x0, dy, y0 * dx);
+    return r;
+  };
+  const double sE = 1.0 - Fm[E_], sN = 1.0 - Fm[N_], sW = 1.0 - Fm[W_], sS = 1.0 - Fm[S_];
+  // survival slopes are -d
+  const Pair sesw = pair(sE, -d[E_], sW, -d[W_]), snss = pair(sN, -d[N_], sS, -d[S_]);
+  const Pair fefw = pair(Fm[E_], d[E_], Fm[W_], d[W_]), fnfs = pair(Fm[N_], d[N_], Fm[S_], d[S_]);
+  const double w1 = GL3::w(1), w0x2 = 2.0 * GL3::w(0);
+  auto term = [&](const Pair& P, const Pair& Q) {
+    const double gs = fma(P.po, Q.po, P.pe * Q.pe);
+    return fma(w0x2, gs, w1 * (P.p0 * Q.p0));
+  };
+  s[0] = term(sesw, snss);
+  s[1] = term(fefw, fnfs);
+  s[2] = term(sesw, fnfs);
+  s[3] = term(snss, fefw);
+}
+
 CPB_D void store(double* pmin, double* pmax, double* psad, int64_t idx, const double acc[4]) {
   if (pmin) pmin[idx] = acc[0];
   if (pmax) pmax[idx] = acc[1];
@@ -170,19 +201,10 @@ CPB_D void uniform_pieces(const double* lo, const double* hi, const double* inv,
       double s[4], F[5], g[4];
       if (FAST) {
         const double tau = half * GL3::x(2);
+        double d[5];
 #pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = al[p];
-        integrands(F, g);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = GL3::w(1) * g[r];
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-#pragma unroll
-          for (int p = 1; p < 5; ++p) F[p] = fma(side ? tau : -tau, be[p], al[p]);
-          integrands(F, g);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(0), g[r], s[r]);
-        }
+        for (int p = 1; p < 5; ++p) d[p] = tau * be[p];
+        gl3_sym_sums(al, d, s);
       } else {
 #pragma unroll
         for (int r = 0; r < 4; ++r) s[r] = 0.0;
@@ -1359,21 +1381,14 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     const double half = 0.5 * (xn - x), mid = 0.5 * (xn + x);
     double s[4];
     if (fast) {
-      double Fm[5], F[5], g[4];
+      double Fm[5], d[5];
       const double tau = half * GL3::x(2);
 #pragma unroll
-      for (int p = 1; p < 5; ++p) Fm[p] = fma(mid - ee[p], ss[p], cc_[p]);
-      integrands(Fm, g);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) s[q] = GL3::w(1) * g[q];
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-#pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = fma(side ? tau : -tau, ss[p], Fm[p]);
-        integrands(F, g);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(0), g[q], s[q]);
+      for (int p = 1; p < 5; ++p) {
+        Fm[p] = fma(mid - ee[p], ss[p], cc_[p]);
+        d[p] = tau * ss[p];
       }
+      gl3_sym_sums(Fm, d, s);
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) s[q] = 0.0;
