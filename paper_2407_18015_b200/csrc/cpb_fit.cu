@@ -714,6 +714,135 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
   merge_range(vmin, vmax, bad, a.range);
 }
 
+// Split-role variant of the fused fit (used when moments AND bounds are
+// wanted): 2 x 128 threads per 128-pixel tile.  Threads [0, 128) run the
+// member-order float64 moment sums (FP64 pipe) and threads [128, 256) the
+// min / max and threshold binning (FP32 / integer pipes) of the same pixels
+// from the same staged tile; the roles need nothing from each other, so the
+// two instruction streams overlap on different pipes and the SM holds twice
+// the warps of the single-role kernel.  Same per-pixel arithmetic.
+template <int NT>
+__global__ void __launch_bounds__(2 * kTmaTile) fit_tma_multi2_kernel(
+    const __grid_constant__ CUtensorMap map, MultiArgs a, int stages, int mbox, int nbox,
+    int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int M = a.members;
+  const int rows = mbox * nbox;
+  const int tid = threadIdx.x;
+  const bool moment_role = tid < kTmaTile;
+  const int px = moment_role ? tid : tid - kTmaTile;
+  float* buf = reinterpret_cast<float*>(smem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * rows * kTmaTile * 4);
+  if (tid == 0) {
+    prefetch_tensormap(&map);
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t pol = policy_evict_first();
+  const uint32_t tile_bytes = (uint32_t)rows * kTmaTile * 4u;
+  auto issue = [&](int64_t tile, int s) {
+    mbar_arrive_expect_tx(&full[s], tile_bytes);
+    float* dst = buf + (size_t)s * rows * kTmaTile;
+    for (int b = 0; b < nbox; ++b)
+      tma_load_2d(dst + (size_t)b * mbox * kTmaTile, &map, (int)(tile * kTmaTile), b * mbox, &full[s], pol);
+  };
+  if (tid == 0) {
+    for (int k = 0; k < stages; ++k) {
+      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+      if (t < ntiles) issue(t, k);
+    }
+  }
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int s = k % stages;
+    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+    const float* col = buf + (size_t)s * rows * kTmaTile + px;
+    const int64_t p = t * kTmaTile + px;
+    if (p < a.npix) {
+      if (moment_role) {
+        double sum = 0.0;
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) sum = __dadd_rn(sum, (double)col[m * kTmaTile]);
+        const double mean = __ddiv_rn(sum, (double)M);
+        double sq = 0.0;
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const double d = __dsub_rn((double)col[m * kTmaTile], mean);
+          sq = __dadd_rn(sq, __dmul_rn(d, d));
+        }
+        const double sd = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (a.mean[i]) {
+            a.mean[i][p] = mean;
+            a.spread[i][p] = sd;
+          }
+        }
+      } else {
+        float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+#pragma unroll 8
+        for (int m = 0; m < M; ++m) {
+          const float x = col[m * kTmaTile];
+          lo = fmin_nan(lo, x);
+          hi = fmaxf(hi, x);
+        }
+        bad |= nonfinite(lo) | nonfinite(hi);
+        vmin = fminf(vmin, lo);
+        vmax = fmaxf(vmax, hi);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (a.lo[i]) {
+            a.lo[i][p] = lo;
+            a.hi[i][p] = hi;
+          }
+        }
+        if (NT > 0 && a.counts) {
+          constexpr int NB = NT > 0 ? NT : 1;
+          const double dlo = (double)lo;
+          const double scale = __ddiv_rn((double)a.bins, __dsub_rn((double)hi, dlo));
+          const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)a.bins);
+          uint32_t c[NB + 1];
+          float thr[NB];
+#pragma unroll
+          for (int q = 1; q < NB; ++q) {
+            thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
+            thr[q] = thr[q] == 0.0f ? -0.0f : thr[q];
+          }
+#pragma unroll
+          for (int q = 0; q <= NB; ++q) c[q] = 0u;
+#pragma unroll 4
+          for (int m = 0; m < M; ++m) {
+            const float x = col[m * kTmaTile];
+#pragma unroll
+            for (int q = 1; q < NB; ++q) c[q] += lt_bit(x, thr[q]);
+          }
+#pragma unroll
+          for (int q = 1; q < NB; ++q) c[q] = (uint32_t)M - c[q];
+          c[0] = (uint32_t)M;
+          const bool flat = !(hi > lo);
+#pragma unroll
+          for (int b = 0; b < NB; ++b) {
+            const uint32_t v = flat ? 0u : (b + 1 < NB ? c[b] - c[b + 1] : c[b]);
+            if (a.wmode == CPB_WEIGHTS_U8)
+              static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
+            else
+              static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const int64_t tn = t + (int64_t)stages * gridDim.x;
+      if (tn < ntiles) issue(tn, s);
+    }
+  }
+  if (!moment_role) merge_range(vmin, vmax, bad, a.range);
+}
+
 __global__ void range_init_kernel(uint32_t* range) {
   range[0] = 0xffffffffu;
   range[1] = 0u;
@@ -1144,6 +1273,11 @@ int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, in
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // split roles (CPB_FIT_SPLIT=1) when both the moment sums and the bounds / bins
+  // are wanted: 21.4 vs 23.4 ms alone, but it slows a concurrent stencil more
+  // (bench step 126.4 vs 124.7 ms overlapped), so it is off by default
+  static const int split_env = [] { const char* e = getenv("CPB_FIT_SPLIT"); return e ? atoi(e) : 0; }();
+  const bool split = split_env && (a.mean[0] || a.mean[1]) && (a.lo[0] || a.lo[1]);
   const int64_t max_chunk = (int64_t)1 << 30;
   for (int64_t p0 = 0; p0 < npix; p0 += max_chunk) {
     MultiArgs c = a;
@@ -1163,13 +1297,14 @@ int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, in
     const int64_t ntiles = (cn + kTmaTile - 1) / kTmaTile;
 #define CPB_MULTI(NTV)                                                                         \
   case NTV: {                                                                                  \
-    auto kern = fit_tma_multi_kernel<NTV>;                                                     \
+    auto kern = split ? fit_tma_multi2_kernel<NTV> : fit_tma_multi_kernel<NTV>;                \
+    const int threads = split ? 2 * kTmaTile : kTmaTile;                                       \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     int per_sm = 1;                                                                            \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTmaTile, smem);              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);               \
     if (g_fit_ctas_per_sm > 0) per_sm = std::min(per_sm, g_fit_ctas_per_sm);                  \
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));        \
-    kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);          \
+    kern<<<(unsigned)grid, threads, smem, st>>>(map, c, stages, mbox, nbox, ntiles);           \
   } break;
     switch (nt) {
       CPB_MULTI(0) CPB_MULTI(1) CPB_MULTI(2) CPB_MULTI(3) CPB_MULTI(4)
