@@ -312,6 +312,24 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(dom["kernel"])
         except Exception:
             traffic = None
+    # the stencils are FP64-bound: their pipe-level figures from the committed
+    # ncu capture (profiles/ncu_fp64.json, tools/ncu_fp64.py)
+    compute = None
+    fpath = os.path.join(ROOT, "profiles", "ncu_fp64.json")
+    if os.path.exists(fpath):
+        try:
+            fp = json.load(open(fpath))
+            key = next((k for k in fp if k.split("<")[0] == dom["kernel"].split("<")[0]), None)
+            if key:
+                r = fp[key]
+                compute = {"bound": "fp64", "kernel": key, "achieved": r["achieved_tflops"],
+                           "peak": r["peak_tflops"], "unit": "TFLOP/s", "frac": r["flop_frac"],
+                           "fp64_inst_frac": r["fp64_inst_frac"],
+                           "fp64_pipe_active_pct": r["fp64_pipe_active_pct"],
+                           "source": "ncu --set full (profiles/ncu_fp64.json); peak = ncu DFMA "
+                                     "peak_sustained x 2 x SM clock"}
+        except Exception:
+            compute = None
     step_bytes = len(models) * (owned_px * 4 * M + st_verts * 24)
     roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": round(dom["gbs"], 1),
                 "peak": hbm, "peak_source": peak_kind, "unit": "GB/s",
@@ -322,7 +340,8 @@ def run_ours(args):
                          "frac": round(step_bytes / (ms_step / 1e3) / 1e9 / hbm, 4),
                          "note": "e2e algorithmic bytes 4M+24 per vertex per model"},
                 "kernels": {f"{k}/{w}": {"ms": round(r["ms"], 3), "GB/s": round(r["gbs"], 1)}
-                            for (k, w), r in kern.items()}}
+                            for (k, w), r in kern.items()},
+                "compute": compute}
     # our kernels per step: range init, fit(s), weight table (histogram),
     # range->pair, pair->eps per field, one stencil per model
     hist = 1 if "histogram" in models else 0
