@@ -227,6 +227,77 @@ CPB_D void uniform_pieces(const double* lo, const double* hi, const double* inv,
   }
 }
 
+// Batcher merge of four sorted (key, tag) pairs: one compare per exchange,
+// the tag (2 (p - 1) + {0: lo, 1: hi}) travels with its key.
+CPB_D void tcswap(double& a, double& b, int& ta, int& tb) {
+  const bool sw = b < a;
+  const double x = sw ? b : a, y = sw ? a : b;
+  const int u = sw ? tb : ta, v = sw ? ta : tb;
+  a = x; b = y; ta = u; tb = v;
+}
+CPB_D void merge_pairs8_tagged(double* k, int* t) {
+  tcswap(k[0], k[2], t[0], t[2]); tcswap(k[1], k[3], t[1], t[3]); tcswap(k[1], k[2], t[1], t[2]);
+  tcswap(k[4], k[6], t[4], t[6]); tcswap(k[5], k[7], t[5], t[7]); tcswap(k[5], k[6], t[5], t[6]);
+  tcswap(k[0], k[4], t[0], t[4]); tcswap(k[1], k[5], t[1], t[5]); tcswap(k[2], k[6], t[2], t[6]);
+  tcswap(k[3], k[7], t[3], t[7]);
+  tcswap(k[2], k[4], t[2], t[4]); tcswap(k[3], k[5], t[3], t[5]);
+  tcswap(k[1], k[2], t[1], t[2]); tcswap(k[3], k[4], t[3], t[4]); tcswap(k[5], k[6], t[5], t[6]);
+}
+
+// uniform_pieces with the piece states tracked from the merge tags: every
+// partition point is some neighbour's (clamped) support end, so crossing it
+// moves that neighbour below -> inside -> above.  A 2-bit crossing count per
+// neighbour replaces the per-piece midpoint comparisons (8 FP64-pipe compares
+// per piece), and the 9 pieces are unrolled so the keys are static registers.
+// Ties are harmless: coincident points bound zero-width pieces, which are
+// skipped, and a count of 2 means "above" whatever the tie order.
+template <bool FAST>
+CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const double* inv,
+                                 const double* k, const int* t, double acc[4]) {
+  double a = lo[C_];
+  unsigned cnt = 0;  // 2 bits per neighbour p at bit 2 (p - 1)
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const double b = i < 8 ? k[i] : hi[C_];
+    if (b > a) {
+      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+      double al[5], be[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        const unsigned c = (cnt >> (2 * (p - 1))) & 3u;
+        const bool in = c == 1u;
+        be[p] = in ? inv[p] : 0.0;
+        al[p] = in ? (FAST ? (mid - lo[p]) * inv[p] : 0.0) : (c == 2u ? 1.0 : 0.0);
+      }
+      double s[4];
+      if (FAST) {
+        const double tau = half * GL3::x(2);
+        double d[5];
+#pragma unroll
+        for (int p = 1; p < 5; ++p) d[p] = tau * be[p];
+        gl3_sym_sums(al, d, s);
+      } else {
+        double F[5], g[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s[r] = 0.0;
+#pragma unroll
+        for (int j = 0; j < GL3::n; ++j) {
+          const double x = node_x(mid, half, GL3::x(j));
+#pragma unroll
+          for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
+          integrands(F, g);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = fma(s[r], half, acc[r]);
+      a = b;
+    }
+    if (i < 8) cnt += 1u << (2 * (t[i] >> 1));
+  }
+}
+
 // One uniform piece [a, b]: s[r] = GL3 sum of integrand r (before half, pdf).
 template <bool FAST>
 CPB_D void uniform_piece(double a, double b, const double* lo, const double* hi, const double* inv,
@@ -289,11 +360,12 @@ CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) 
     k[2 * p - 2] = dmin(dmax(lo[p], lo[C_]), hi[C_]);
     k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
   }
-  merge_pairs8(k);
+  int t[8] = {0, 1, 2, 3, 4, 5, 6, 7};
+  merge_pairs8_tagged(k, t);
 #pragma unroll
   for (int r = 0; r < 4; ++r) acc[r] = 0.0;
-  if (fast) uniform_pieces<true>(lo, hi, inv, k, acc);
-  else uniform_pieces<false>(lo, hi, inv, k, acc);
+  if (fast) uniform_pieces_tagged<true>(lo, hi, inv, k, t, acc);
+  else uniform_pieces_tagged<false>(lo, hi, inv, k, t, acc);
 #pragma unroll
   for (int r = 0; r < 4; ++r) acc[r] *= inv[C_];
 }
