@@ -628,6 +628,57 @@ CPB_D void epan_piece(double a, double b, const double* m, const double* ih, con
   range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
 }
 
+// epan_piece with the neighbour states given (2 bits each, from the merge
+// tags: 0 below, 1 inside, 2 above) instead of midpoint comparisons.
+template <bool FAST>
+CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, unsigned state,
+                         double s[4]) {
+  const double pdf0 = 0.75 * ih[C_];
+  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+  double al[5], be[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    const unsigned c = (state >> (2 * (p - 1))) & 3u;
+    const bool in = c == 1u;
+    be[p] = in ? ih[p] : 0.0;
+    al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (c == 2u ? 1.0 : -1.0);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) s[r] = 0.0;
+  if (FAST) {
+    const double uc0 = (mid - m[C_]) * ih[C_];
+#pragma unroll
+    for (int j = 0; j < GL8::n / 2; ++j) {
+      const double tau = half * GL8::x(7 - j);
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const double t = side ? tau : -tau;
+        const double uc = fma(t, ih[C_], uc0);
+        const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+        double F[5], g[4];
+#pragma unroll
+        for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
+        integrands(F, g);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < GL8::n; ++j) {
+      const double x = node_x(mid, half, GL8::x(j));
+      const double uc = (x - m[C_]) * ih[C_];
+      const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+      double F[5], g[4];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
+      integrands(F, g);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+    }
+  }
+}
+
 // Piece-parallel Epanechnikov stencil.  With one vertex per lane, a warp
 // iterates over the UNION of its lanes' pieces (9 on smooth fields) although a
 // vertex has ~5 non-empty pieces, so ~45 % of the 8-node piece evaluations are
@@ -645,6 +696,7 @@ struct PPWarpSmem {
   double pa[9 * 32], pb[9 * 32];
   double res[9 * 32][3];  // per piece: min, max, saddle (t1 + t2)
   unsigned char owner[9 * 32];
+  unsigned char state[9 * 32];  // per piece: 2-bit below / inside / above state of E, N, W, S
   unsigned char fast[32];
 };
 
@@ -877,6 +929,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   int64_t idx = 0;
   int n = 0;
   double pts[10];
+  int tg[8];
   if (live) {
     const int64_t r = row_begin + v / cols, c = 1 + v % cols;
     idx = r * f.width + c;
@@ -922,7 +975,9 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
       k[2 * p - 2] = dmin(dmax(lo[p], lo[C_]), hi[C_]);
       k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
     }
-    merge_pairs8(k);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tg[q] = q;
+    merge_pairs8_tagged(k, tg);
     pts[0] = lo[C_];
 #pragma unroll
     for (int q = 0; q < 8; ++q) pts[q + 1] = k[q];
@@ -941,14 +996,17 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   off -= n;
   if (live) {
     int q = off;
+    unsigned cnt = 0;  // crossing counts of the partition points so far (2 bits per neighbour)
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
       if (pts[i + 1] > pts[i]) {
         S.pa[q] = pts[i];
         S.pb[q] = pts[i + 1];
         S.owner[q] = (unsigned char)lane;
+        S.state[q] = (unsigned char)cnt;
         ++q;
       }
+      if (i < 8) cnt += 1u << (2 * (tg[i] >> 1));
     }
   }
   __syncwarp();
@@ -968,19 +1026,16 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
       if (S.fast[o]) uniform_piece<true>(a, b, lo, hi, inv, s, mk);
       else uniform_piece<false>(a, b, lo, hi, inv, s, mk);
     } else {
-      double m[5], ih[5], lo[5], hi[5];
+      double m[5], ih[5];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
         m[p] = S.vd[p][o];
         ih[p] = S.vd[5 + p][o];
       }
-#pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        lo[p] = S.vd[9 + p][o];
-        hi[p] = S.vd[13 + p][o];
-      }
-      if (S.fast[o]) epan_piece<true>(a, b, m, ih, lo, hi, s, mk);
-      else epan_piece<false>(a, b, m, ih, lo, hi, s, mk);
+      const unsigned st = S.state[e];
+      if (S.fast[o]) epan_piece_st<true>(a, b, m, ih, st, s);
+      else epan_piece_st<false>(a, b, m, ih, st, s);
+      mk[0] = mk[1] = mk[2] = mk[3] = true;
     }
     const double half = 0.5 * (b - a);
 #pragma unroll
