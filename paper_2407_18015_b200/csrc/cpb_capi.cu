@@ -554,8 +554,14 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
       if (e != cudaSuccess) return cuda_status(e, "event wait");
     }
     const size_t off = (size_t)r0 * width;
+    // one pass over the chunk for all models (cpb_fit_multi); the shared data
+    // range accumulates in model 0's range words
+    cpb_field fcs[16];
+    cpb_field* fptr[16];
+    uint32_t* rng0 = (uint32_t*)planes[0][6].p;
     for (int i = 0; i < nm; ++i) {
-      cpb_field fc = fm[i];
+      cpb_field& fc = fcs[i];
+      fc = fm[i];
       fc.height = nr;
       fc.lo = pb[i][0] ? (char*)planes[i][0].p + off * sizeof(float) : nullptr;
       fc.hi = pb[i][1] ? (char*)planes[i][1].p + off * sizeof(float) : nullptr;
@@ -565,13 +571,15 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
       // keeps the full-grid plane stride
       fc.weights = pb[i][4] ? (char*)planes[i][4].p + off * (members <= 255 ? 1 : 2) : nullptr;
       fc.plane_stride = (int64_t)plane;
-      if ((s = cpb_fit((const float*)ebuf[b].p, (int64_t)nr * width, &fc,
-                       (uint32_t*)planes[i][6].p, j > 0, st)))
-        return s;
-      fm[i].bounds = fc.bounds;
-      fm[i].weights_mode = fc.weights_mode;
+      fptr[i] = &fc;
+    }
+    if ((s = cpb_fit_multi((const float*)ebuf[b].p, (int64_t)nr * width, fptr, nm, rng0, j > 0, st)))
+      return s;
+    for (int i = 0; i < nm; ++i) {
+      fm[i].bounds = fcs[i].bounds;
+      fm[i].weights_mode = fcs[i].weights_mode;
       // provisional eps of the rows fitted so far (exact once the last chunk is in)
-      if ((s = cpb_range_to_pair((const uint32_t*)planes[i][6].p, (double*)pair[i].p, st)) ||
+      if ((s = cpb_range_to_pair(rng0, (double*)pair[i].p, st)) ||
           (s = cpb_pair_to_eps((const double*)pair[i].p, (double*)epsbuf[i].p + j, st)))
         return s;
     }
