@@ -1429,31 +1429,8 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   const int tid = threadIdx.y * kTabTW + threadIdx.x;
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const double dh = (double)h, invM = 1.0 / (double)f.members;
-  for (int i = tid; i < P; i += kTabTW * kTabTH) {
-    const int64_t rr = r0 - 1 + i / SW, cc = c0 + i % SW;
-    if (rr >= f.height || cc >= f.width) continue;
-    const int64_t at = rr * f.width + cc;
-    double lo, hi;
-    const bool deg = load_bounds(f, at, lo, hi);
-    const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at), lo, hi, h) : 0;
-    double wv[HB];
-#pragma unroll
-    for (int b = 0; b < HB; ++b) {
-      double wb = 0.0;
-      if (b < h) {
-        if (f.wmode == CPB_WEIGHTS_F64) {
-          wb = __ldg(static_cast<const double*>(f.weights) + (int64_t)b * f.wstride + at);
-        } else if (deg) {
-          wb = b == dbin ? 1.0 : 0.0;
-        } else {
-          const unsigned cnt = f.wmode == CPB_WEIGHTS_U8
-              ? (unsigned)__ldg(static_cast<const uint8_t*>(f.weights) + (int64_t)b * f.wstride + at)
-              : (unsigned)__ldg(static_cast<const uint16_t*>(f.weights) + (int64_t)b * f.wstride + at);
-          wb = (double)cnt * invM;  // count / M to within an ulp (closed-form tolerance)
-        }
-      }
-      wv[b] = wb;
-    }
+  // per-pixel state tables from (lo, hi, raw weights)
+  auto build = [&](int i, double lo, double hi, const double* wv) {
     const double it = 1.0 / (HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
     T[0 * P + i] = 0.0; T[1 * P + i] = 0.0; T[2 * P + i] = 0.0; T[3 * P + i] = lo;
@@ -1473,6 +1450,77 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     double* t = T + (size_t)(h + 1) * 4 * P + i;
     t[0] = 1.0; t[P] = 0.0; t[2 * P] = 0.0; t[3 * P] = inf;
     RATIO[i] = (fabs(lo) + fabs(hi)) * ibinw;
+  };
+  constexpr int NT = kTabTW * kTabTH, NPT = (P + NT - 1) / NT;
+  if (HB <= 8 && f.bounds == CPB_BOUNDS_F32_FITTED && f.wmode == CPB_WEIGHTS_U8) {
+    // fitted planes (the common case): issue every global load of this
+    // thread's pixels first, then build -- one exposed load latency, not NPT
+    constexpr int HC = HB <= 8 ? HB : 1;
+    float rlo[NPT], rhi[NPT];
+    unsigned rc[NPT][HC];
+    int64_t at[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      const int i = tid + j * NT;
+      const int64_t rr = r0 - 1 + i / SW, cc = c0 + i % SW;
+      at[j] = (i < P && rr < f.height && cc < f.width) ? rr * f.width + cc : -1;
+      rlo[j] = rhi[j] = 0.0f;
+      if (at[j] >= 0) {
+        rlo[j] = __ldg(static_cast<const float*>(f.lo) + at[j]);
+        rhi[j] = __ldg(static_cast<const float*>(f.hi) + at[j]);
+      }
+#pragma unroll
+      for (int q = 0; q < HC; ++q)
+        rc[j][q] = at[j] >= 0 ? (unsigned)__ldg(static_cast<const uint8_t*>(f.weights) + (int64_t)q * f.wstride + at[j]) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      if (at[j] < 0) continue;
+      double lo = (double)rlo[j], hi = (double)rhi[j];
+      const bool deg = !(hi > lo);
+      int dbin = 0;
+      if (deg) {  // load_bounds: widen by eps/2 at use (fields.py:140-143)
+        const double c = lo, hh = __dmul_rn(0.5, field_eps(f));
+        lo = __dsub_rn(c, hh);
+        hi = __dadd_rn(c, hh);
+        dbin = degenerate_bin(c, lo, hi, h);
+      }
+      double wv[HB];
+#pragma unroll
+      for (int q = 0; q < HB; ++q) {
+        const unsigned cnt = rc[j][q < HC ? q : 0];
+        wv[q] = q < h ? (deg ? (q == dbin ? 1.0 : 0.0) : (double)cnt * invM) : 0.0;
+      }
+      build(tid + j * NT, lo, hi, wv);
+    }
+  } else {
+    for (int i = tid; i < P; i += NT) {
+      const int64_t rr = r0 - 1 + i / SW, cc = c0 + i % SW;
+      if (rr >= f.height || cc >= f.width) continue;
+      const int64_t at = rr * f.width + cc;
+      double lo, hi;
+      const bool deg = load_bounds(f, at, lo, hi);
+      const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at), lo, hi, h) : 0;
+      double wv[HB];
+#pragma unroll
+      for (int b = 0; b < HB; ++b) {
+        double wb = 0.0;
+        if (b < h) {
+          if (f.wmode == CPB_WEIGHTS_F64) {
+            wb = __ldg(static_cast<const double*>(f.weights) + (int64_t)b * f.wstride + at);
+          } else if (deg) {
+            wb = b == dbin ? 1.0 : 0.0;
+          } else {
+            const unsigned cnt = f.wmode == CPB_WEIGHTS_U8
+                ? (unsigned)__ldg(static_cast<const uint8_t*>(f.weights) + (int64_t)b * f.wstride + at)
+                : (unsigned)__ldg(static_cast<const uint16_t*>(f.weights) + (int64_t)b * f.wstride + at);
+            wb = (double)cnt * invM;  // count / M to within an ulp (closed-form tolerance)
+          }
+        }
+        wv[b] = wb;
+      }
+      build(i, lo, hi, wv);
+    }
   }
   __syncthreads();
   const int64_t r = r0 + threadIdx.y, c = c0 + 1 + threadIdx.x;
