@@ -71,6 +71,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--serial", action="store_true", help="no fit/stencil overlap (one stream)")
+    p.add_argument("--concurrent-stencils", action="store_true",
+                   help="run the models' stencils on separate streams (one output buffer each)")
     p.add_argument("--fit", choices=("fused", "separate"), default="fused",
                    help="fused: one cpb_fit_multi pass over the ensemble for all models per step; "
                         "separate: one cpb_fit per model")
@@ -208,6 +210,11 @@ def run_ours(args):
         fitted = [torch.cuda.Event() for _ in range(nsets)]
         consumed = [torch.cuda.Event() for _ in range(nsets)]
         counter = [0]
+        conc = args.concurrent_stencils
+        if conc:
+            s_model = {k: torch.cuda.Stream(device=device, priority=0) for k in models}
+            outs = {k: torch.zeros((3, slab.local_height, W), dtype=torch.float64, device=device)
+                    for k in models}
 
         def step():
             b = counter[0] % nsets
@@ -219,15 +226,28 @@ def run_ours(args):
                     s_fit.wait_event(consumed[b])
                 D.fit_slab_fields([fs[k] for k in models], ens, timer=timer)
                 fitted[b].record()
-            with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
-                if overlap:
-                    s_cls.wait_event(fitted[b])
+            if conc:
+                # each model's stencil on its own stream: the load-latency-bound
+                # uniform and the FP64-bound stencils share the SMs
                 for kind in models:
-                    timer.kind = kind
-                    _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=out, sums=True,
-                                                    timer=timer)
-                consumed[b].record()
-            if overlap:
+                    sk = s_model[kind]
+                    sk.wait_event(fitted[b])
+                    with torch.cuda.stream(sk):
+                        timer.kind = kind
+                        _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=outs[kind],
+                                                        sums=True, timer=timer)
+                    s_cls.wait_stream(sk)
+                s_cls.record_event(consumed[b])
+            else:
+                with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
+                    if overlap:
+                        s_cls.wait_event(fitted[b])
+                    for kind in models:
+                        timer.kind = kind
+                        _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=out, sums=True,
+                                                        timer=timer)
+                    consumed[b].record()
+            if overlap or conc:
                 torch.cuda.current_stream().wait_stream(s_cls)
     else:
         # one reusable halo-padded field per model; eps stays on the device, so the
