@@ -229,9 +229,10 @@ class SlabField:
         return self.dev
 
 
-def fit_slab_fields(fields, ens_slab, group=None, timer=None):
+def fit_slab_fields(fields, ens_slab, group=None, timer=None, finish: bool = True):
     """Fit several SlabFields of one slab in a single pass over the ensemble
-    (cpb_fit_multi); then the shared global eps and each field's halo exchange."""
+    (cpb_fit_multi); then (``finish``) the shared global eps and each field's
+    halo exchange (finish_slab_fields)."""
     import ctypes
 
     from . import _lib
@@ -251,7 +252,25 @@ def fit_slab_fields(fields, ens_slab, group=None, timer=None):
         st = f.dev.struct
         st.bounds, st.weights_mode, st.plane_stride = f.view.bounds, f.view.weights_mode, 0
     if all(f.device_eps for f in fields):
+        # this slab's {-min, max} pair, on the device
         _lib.check(lib.cpb_range_to_pair(rng, f0.pair.data_ptr(), s))
+    if finish:
+        finish_slab_fields(fields, group)
+    return [f.dev for f in fields]
+
+
+def finish_slab_fields(fields, group=None):
+    """Second half of fit_slab_fields: MAX all-reduce of the {-min, max} pair
+    (NCCL), the global eps written where the stencils read it, and the halo
+    rows of every plane from the neighbouring ranks."""
+    import ctypes
+
+    from . import _lib
+
+    lib = _lib.load()
+    s = _lib.stream_ptr()
+    f0 = fields[0]
+    if all(f.device_eps for f in fields):
         _, world = _group_world(group)
         if world > 1:
             import torch.distributed as dist
@@ -260,14 +279,14 @@ def fit_slab_fields(fields, ens_slab, group=None, timer=None):
         for f in fields:
             _lib.check(lib.cpb_pair_to_eps(f0.pair.data_ptr(), f.eps_t.data_ptr(), s))
     else:
+        rng = f0.dev.tensors["range"].data_ptr()
         gmin, gmax = ctypes.c_double(), ctypes.c_double()
         _lib.check(lib.cpb_read_range(rng, ctypes.byref(gmin), ctypes.byref(gmax), s))
-        gmin, gmax = allreduce_range(gmin.value, gmax.value, ens_slab.device, group)
+        gmin, gmax = allreduce_range(gmin.value, gmax.value, f0.pair.device, group)
         for f in fields:
             f.dev.eps = lib.cpb_epsilon(gmin, gmax)
     for f in fields:
         exchange_halo_rows(_plane_views(f.dev), f.slab, group)
-    return [f.dev for f in fields]
 
 
 def fit_slab(ens_slab, model, slab: Slab, width: int, group=None, timer=None):

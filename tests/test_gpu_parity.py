@@ -503,3 +503,50 @@ def test_fit_multi_matches_separate_fits():
                 p = cpb.classify_field(f)
                 q = cpb.classify_field(cpb.UncertainField.from_ensemble(stack, m))
                 assert np.array_equal(p.p_min, q.p_min) and np.array_equal(p.p_saddle, q.p_saddle)
+
+
+def test_row_slabs_on_device_match_single_gpu():
+    """The multi-GPU path's device side (SlabField views, fused slab fit, the
+    {-min, max} pair -> global eps, halo rows, stencil rows, global pixel keys)
+    for G = 3 slabs run one after another on this GPU.  The two collectives are
+    emulated in-process: the MAX of the slabs' pairs and copies of the boundary
+    rows between the slabs' planes (what NCCL does across ranks)."""
+    from paper_2407_18015_b200 import distributed as D
+
+    H, W, M, G = 23, 31, 12, 3
+    vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=4)
+    vals[:, 11, 7] = 0.5  # a degenerate pixel: needs the GLOBAL eps
+    dev = torch.device("cuda")
+    models = [cpb.ModelSpec("uniform"), cpb.ModelSpec("epanechnikov"), cpb.ModelSpec("histogram", bins=5)]
+    slabs = [D.slab_rows(H, r, G) for r in range(G)]
+    fields = [[D.SlabField(m, s, W, M, dev) for m in models] for s in slabs]
+    for s, fs in zip(slabs, fields):
+        ens = torch.as_tensor(np.ascontiguousarray(vals[:, s.row_begin:s.row_end]), device=dev)
+        D.fit_slab_fields(fs, ens, finish=False)
+    pair = torch.stack([fs[0].pair for fs in fields]).max(dim=0).values  # NCCL MAX all-reduce
+    for fs in fields:
+        fs[0].pair.copy_(pair)
+        D.finish_slab_fields(fs)  # world 1 here: eps only
+    for r in range(G - 1):  # halo rows: last owned row down, first owned row up
+        lo_s, hi_s = slabs[r], slabs[r + 1]
+        for fa, fb in zip(fields[r], fields[r + 1]):
+            for pa, pb in zip(D._plane_views(fa.dev), D._plane_views(fb.dev)):
+                last = lo_s.halo_top + lo_s.owned - 1
+                pb[..., 0, :].copy_(pa[..., last, :])
+                pa[..., last + 1, :].copy_(pb[..., hi_s.halo_top, :])
+    torch.cuda.synchronize()
+    stack = cpb.EnsembleStack(vals)
+    for i, m in enumerate(models):
+        full = cpb.UncertainField.from_ensemble(stack, m)
+        ref_c = cpb.classify_field(full)
+        est = cpb.EstimatorSpec("monte_carlo", n_samples=300, seed=6)
+        ref_m = cpb.classify_field(full, est)
+        for s, fs in zip(slabs, fields):
+            a, b = s.stencil_rows()
+            g0 = s.local_row0
+            out, _ = D.classify_slab(fs[i].dev, s, cpb.EstimatorSpec())
+            outm, _ = D.classify_slab(fs[i].dev, s, est)
+            for c, ch in enumerate(("min", "max", "saddle")):
+                got = out[c, a:b].cpu().numpy()
+                assert np.array_equal(got, ref_c.channel(ch)[g0 + a:g0 + b]), (m.kind, ch)
+                assert np.array_equal(outm[c, a:b].cpu().numpy(), ref_m.channel(ch)[g0 + a:g0 + b]), (m.kind, ch)
