@@ -489,14 +489,15 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
   // per-chunk events (the ring events are reused, so the stencil stream waits on its own copy)
   std::vector<cudaEvent_t> fitted((size_t)nchunks, nullptr), classified((size_t)nchunks, nullptr);
   struct EvVec {
-    std::vector<cudaEvent_t>* a; std::vector<cudaEvent_t>* b; cudaStream_t c1, c2;
-    ~EvVec() {  // destroyed before the buffers: drain the stencil and copy streams first
-      if (c1) cudaStreamSynchronize(c1);
-      if (c2) cudaStreamSynchronize(c2);
+    std::vector<cudaEvent_t>* a; std::vector<cudaEvent_t>* b; cudaStream_t st[4];
+    ~EvVec() {  // destroyed before the buffers: drain every stream first (also on
+                // an error return, when work may still be queued on any of them)
+      for (cudaStream_t x : st)
+        if (x) cudaStreamSynchronize(x);
       for (auto* v : {a, b})
         for (auto ev : *v) if (ev) cudaEventDestroy(ev);
     }
-  } evguard{&fitted, &classified, scls, scopy};
+  } evguard{&fitted, &classified, {ss.s[0], ss.s[1], scls, scopy}};
   for (int64_t j = 0; j < nchunks; ++j) {
     e = cudaEventCreateWithFlags(&fitted[j], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&classified[j], cudaEventDisableTiming);
