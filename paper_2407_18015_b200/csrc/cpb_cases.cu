@@ -554,13 +554,24 @@ int launch_cases_mc(const cpb_case_batch* b, uint64_t seed, const uint64_t* pixe
     set_error("n_cases * n too large for one launch");
     return CPB_EINVAL;
   }
+  const size_t smem = (size_t)kMaxPos * (2 * B.maxb + 1) * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_error("too many histogram bins (%d) for the per-case sampler tables", B.maxb);
+    return CPB_EINVAL;
+  }
+  // caller-provided counts, or stream-ordered scratch from the library pool
+  struct Scratch {
+    unsigned long long* p = nullptr;
+    cudaStream_t st;
+    ~Scratch() { workspace_free(p, st); }
+  } scratch{nullptr, st};
   unsigned long long* cnt = counts;
   if (!cnt) {
-    if (int s = workspace_alloc((void**)&cnt, (size_t)B.n * 3 * sizeof(unsigned long long), st)) return s;
+    if (int s = workspace_alloc((void**)&scratch.p, (size_t)B.n * 3 * sizeof(unsigned long long), st)) return s;
+    cnt = scratch.p;
   }
   cudaError_t e = cudaMemsetAsync(cnt, 0, (size_t)B.n * 3 * sizeof(unsigned long long), st);
   if (e != cudaSuccess) return cuda_status(e, "memset counts");
-  const size_t smem = (size_t)kMaxPos * (2 * B.maxb + 1) * sizeof(double);
   auto kern = B.k == 2 ? cases_mc_kernel<2> : cases_mc_kernel<4>;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -568,7 +579,6 @@ int launch_cases_mc(const cpb_case_batch* b, uint64_t seed, const uint64_t* pixe
   CPB_CHECK_LAUNCH("per-case Monte Carlo kernel");
   cases_finish_kernel<<<(unsigned)((3 * B.n + 255) / 256), 256, 0, st>>>(cnt, B.n, n, out);
   CPB_CHECK_LAUNCH("per-case Monte Carlo finish");
-  if (!counts) workspace_free(cnt, st);
   return CPB_OK;
 }
 
@@ -582,6 +592,10 @@ int launch_cases_semi(const cpb_case_batch* b, uint64_t seed, const uint64_t* pi
   if (b->n_cases == 0) return CPB_OK;
   const Batch B = make_batch(*b);
   const size_t smem = ((size_t)kMaxPos * (2 * B.maxb + 1) + B.maxb + 1) * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_error("too many histogram bins (%d) for the per-case semianalytical tables", B.maxb);
+    return CPB_EINVAL;
+  }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(cases_semi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cases_semi_kernel<<<(unsigned)B.n, kCombThreads, smem, st>>>(B, seed, pixels, c, out);
