@@ -71,6 +71,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--serial", action="store_true", help="no fit/stencil overlap (one stream)")
+    p.add_argument("--fit-priority", choices=("high", "low"), default="high",
+                   help="stream priority of the (overlapped) fit relative to the stencils")
     p.add_argument("--concurrent-stencils", action="store_true",
                    help="run the models' stencils on separate streams (one output buffer each)")
     p.add_argument("--fit", choices=("fused", "separate"), default="fused",
@@ -196,8 +198,11 @@ def run_ours(args):
         from paper_2407_18015_b200 import _lib
 
         _lib.check(_lib.load().cpb_set_option(b"fit_ctas_per_sm", args.fit_ctas))
-    s_fit = torch.cuda.Stream(device=device, priority=-1)
-    s_cls = torch.cuda.Stream(device=device, priority=0)
+    # stream priorities (lower = higher priority); --fit-priority low lets the
+    # stencils keep the SMs and the next step's fit fill the gaps
+    fit_hi = args.fit_priority == "high"
+    s_fit = torch.cuda.Stream(device=device, priority=-1 if fit_hi else 0)
+    s_cls = torch.cuda.Stream(device=device, priority=0 if fit_hi else -1)
     fused = args.fit == "fused" and len(models) > 1
     if fused:
         # all models fitted in ONE pass over the ensemble (cpb_fit_multi); two
