@@ -376,8 +376,37 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
   if (!vertex(f, w, idx)) return;
   const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
   double lo[5], hi[5];
+  if (f.bounds == CPB_BOUNDS_F32_FITTED) {
+    // all ten loads in flight before any use, then the eps widening of
+    // degenerate pixels (load_bounds)
+    float rl[5], rh[5];
 #pragma unroll
-  for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+    for (int p = 0; p < 5; ++p) {
+      rl[p] = __ldg(static_cast<const float*>(f.lo) + at[p]);
+      rh[p] = __ldg(static_cast<const float*>(f.hi) + at[p]);
+    }
+    bool deg = false;
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      lo[p] = (double)rl[p];
+      hi[p] = (double)rh[p];
+      deg |= !(hi[p] > lo[p]);
+    }
+    if (deg) {
+      const double he = __dmul_rn(0.5, field_eps(f));
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        if (!(hi[p] > lo[p])) {
+          const double c = lo[p];
+          lo[p] = __dsub_rn(c, he);
+          hi[p] = __dadd_rn(c, he);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+  }
   double acc[4];
   uniform_integrals(lo, hi, acc);
   store(pmin, pmax, psad, idx, acc);
