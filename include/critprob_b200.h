@@ -187,6 +187,14 @@ int cpb_from_scalar(const double* d_values, int64_t height, int64_t width, doubl
 int cpb_classify_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
                         double* d_pmax, double* d_psaddle, void* stream);
 
+/* cpb_classify_closed plus the expected per-type counts of the launch's
+ * vertices (sum of p_min, p_max, p_saddle over rows [row_begin, row_end)),
+ * ADDED to d_counts[0..2] (3 device doubles): fused into the stencil kernels'
+ * epilogue (per-block partials, summed in block order: deterministic). */
+int cpb_classify_closed_counts(const cpb_field* f, int64_t row_begin, int64_t row_end,
+                               double* d_pmin, double* d_pmax, double* d_psaddle, double* d_counts,
+                               void* stream);
+
 /*
  * Monte Carlo pattern fractions (engine.py:195-222, 632-666): n_samples joint
  * inverse-CDF draws per vertex, strict comparisons, p = count / n.  With

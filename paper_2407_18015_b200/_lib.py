@@ -61,6 +61,8 @@ _SIGNATURES = {
     "cpb_pair_to_eps": (c_i32, [c_vp, c_vp, c_vp]),
     "cpb_from_scalar": (c_i32, [c_vp, c_i64, c_i64, c_dbl, c_dbl, c_vp, c_vp, c_vp]),
     "cpb_classify_closed": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "cpb_classify_closed_counts": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+                                           c_vp]),
     "cpb_classify_mc": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_u64, c_i64, c_i32,
                                 c_vp, c_vp, c_vp, c_vp, c_vp]),
     "cpb_classify_semi": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_u64, c_i64, c_vp, c_vp,

@@ -25,7 +25,7 @@ int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cuda
 int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
                  int64_t height, double amp, uint64_t seed, cudaStream_t st);
 int launch_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, double* pmin,
-                  double* pmax, double* psad, cudaStream_t st);
+                  double* pmax, double* psad, cudaStream_t st, double* counts);
 int launch_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed, int64_t n,
               int rng, double* pmin, double* pmax, double* psad, int64_t* counts, cudaStream_t st);
 int launch_unit_block(uint64_t seed, const uint64_t* px, int64_t npix, int planes, int64_t start,
@@ -231,7 +231,27 @@ int cpb_classify_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, 
       return CPB_EINVAL;
     }
   }
-  return launch_closed(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle, (cudaStream_t)stream);
+  return launch_closed(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle, (cudaStream_t)stream, nullptr);
+}
+
+int cpb_classify_closed_counts(const cpb_field* f, int64_t row_begin, int64_t row_end,
+                               double* d_pmin, double* d_pmax, double* d_psaddle, double* d_counts,
+                               void* stream) {
+  if (!d_counts) { set_error("d_counts must not be NULL"); return CPB_EINVAL; }
+  int s = check_field(f, true);
+  if (s) return s;
+  if (f->kind == CPB_GAUSSIAN) {
+    set_error("Gaussian fields have no closed form; use monte_carlo");
+    return CPB_EINVAL;
+  }
+  if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
+    if (row_end > row_begin) {
+      set_error("rows [%lld, %lld) need a one-row halo inside the field",
+                (long long)row_begin, (long long)row_end);
+      return CPB_EINVAL;
+    }
+  }
+  return launch_closed(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle, (cudaStream_t)stream, d_counts);
 }
 
 int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,

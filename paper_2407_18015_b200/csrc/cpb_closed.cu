@@ -18,6 +18,8 @@
 // the reference's own grid-vs-case tolerance, test_engine.py:548-559).
 #include <stdlib.h>
 
+#include <algorithm>
+
 #include "cpb_common.cuh"
 
 namespace cpb {
@@ -111,6 +113,89 @@ CPB_D void store(double* pmin, double* pmax, double* psad, int64_t idx, const do
   if (pmin) pmin[idx] = acc[0];
   if (pmax) pmax[idx] = acc[1];
   if (psad) psad[idx] = acc[2] + acc[3];
+}
+
+// Expected per-type counts (sum of each channel over the launch's vertices,
+// SURVEY.md §8 e): every WARP reduces its lanes' (p_min, p_max, p_saddle) with
+// a fixed shuffle tree and writes one partial triple (no block barrier, so
+// warps still retire independently); counts_reduce_kernel and
+// counts_finish_kernel add the partials with a fixed tree.  Deterministic for
+// a given launch shape.  Every lane of a warp must call it (dead lanes pass 0).
+CPB_D void warp_partial_sums(double v0, double v1, double v2, double* partial) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, d);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, d);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, d);
+  }
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  const int wpb = (blockDim.x * blockDim.y + 31) / 32;
+  if ((tid & 31) == 0) {
+    const int64_t w = ((int64_t)blockIdx.x + (int64_t)blockIdx.y * gridDim.x) * wpb + (tid >> 5);
+    partial[3 * w] = v0;
+    partial[3 * w + 1] = v1;
+    partial[3 * w + 2] = v2;
+  }
+}
+
+constexpr int kCountChunks = 1024;
+
+// stage 1: chunk c of the warp partials -> chunk[c] (fixed tree per block)
+__global__ void counts_reduce_kernel(const double* partial, int64_t n, double* chunk) {
+  __shared__ double red[256][3];
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = (int64_t)blockIdx.x * per, b1 = b0 + per < n ? b0 + per : n;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int64_t b = b0 + threadIdx.x; b < b1; b += 256) {
+    a0 += partial[3 * b];
+    a1 += partial[3 * b + 1];
+    a2 += partial[3 * b + 2];
+  }
+  red[threadIdx.x][0] = a0;
+  red[threadIdx.x][1] = a1;
+  red[threadIdx.x][2] = a2;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int c = 0; c < 3; ++c) red[threadIdx.x][c] += red[threadIdx.x + w][c];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) chunk[3 * blockIdx.x + threadIdx.x] = red[0][threadIdx.x];
+}
+
+// stage 2: the chunks -> counts[0..2] (added)
+__global__ void counts_finish_kernel(const double* chunk, int64_t n, double* counts) {
+  __shared__ double red[256][3];
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (int64_t b = threadIdx.x; b < n; b += 256) {
+    a0 += chunk[3 * b];
+    a1 += chunk[3 * b + 1];
+    a2 += chunk[3 * b + 2];
+  }
+  red[threadIdx.x][0] = a0;
+  red[threadIdx.x][1] = a1;
+  red[threadIdx.x][2] = a2;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int c = 0; c < 3; ++c) red[threadIdx.x][c] += red[threadIdx.x + w][c];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) counts[threadIdx.x] += red[0][threadIdx.x];
+}
+
+__global__ void rows_partial_kernel(const double* pmin, const double* pmax, const double* psad,
+                                    int64_t row_begin, int64_t cols, int64_t width, int64_t nvert,
+                                    double* partial) {
+  double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvert;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t idx = (row_begin + v / cols) * width + 1 + v % cols;
+    if (pmin) v0 += pmin[idx];
+    if (pmax) v1 += pmax[idx];
+    if (psad) v2 += psad[idx];
+  }
+  warp_partial_sums(v0, v1, v2, partial);
 }
 
 struct Window {
@@ -371,45 +456,48 @@ CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) 
 }
 
 __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
-    FieldView f, Window w, double* pmin, double* pmax, double* psad) {
-  int64_t idx;
-  if (!vertex(f, w, idx)) return;
-  const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
-  double lo[5], hi[5];
-  if (f.bounds == CPB_BOUNDS_F32_FITTED) {
-    // all ten loads in flight before any use, then the eps widening of
-    // degenerate pixels (load_bounds)
-    float rl[5], rh[5];
-#pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      rl[p] = __ldg(static_cast<const float*>(f.lo) + at[p]);
-      rh[p] = __ldg(static_cast<const float*>(f.hi) + at[p]);
-    }
-    bool deg = false;
-#pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      lo[p] = (double)rl[p];
-      hi[p] = (double)rh[p];
-      deg |= !(hi[p] > lo[p]);
-    }
-    if (deg) {
-      const double he = __dmul_rn(0.5, field_eps(f));
+    FieldView f, Window w, double* pmin, double* pmax, double* psad, double* partial) {
+  int64_t idx = 0;
+  const bool live = vertex(f, w, idx);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (live) {
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    double lo[5], hi[5];
+    if (f.bounds == CPB_BOUNDS_F32_FITTED) {
+      // all ten loads in flight before any use, then the eps widening of
+      // degenerate pixels (load_bounds)
+      float rl[5], rh[5];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
-        if (!(hi[p] > lo[p])) {
-          const double c = lo[p];
-          lo[p] = __dsub_rn(c, he);
-          hi[p] = __dadd_rn(c, he);
+        rl[p] = __ldg(static_cast<const float*>(f.lo) + at[p]);
+        rh[p] = __ldg(static_cast<const float*>(f.hi) + at[p]);
+      }
+      bool deg = false;
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        lo[p] = (double)rl[p];
+        hi[p] = (double)rh[p];
+        deg |= !(hi[p] > lo[p]);
+      }
+      if (deg) {
+        const double he = __dmul_rn(0.5, field_eps(f));
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+          if (!(hi[p] > lo[p])) {
+            const double c = lo[p];
+            lo[p] = __dsub_rn(c, he);
+            hi[p] = __dadd_rn(c, he);
+          }
         }
       }
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+      for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+    }
+    uniform_integrals(lo, hi, acc);
+    store(pmin, pmax, psad, idx, acc);
   }
-  double acc[4];
-  uniform_integrals(lo, hi, acc);
-  store(pmin, pmax, psad, idx, acc);
+  if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
 }
 
 // --------------------------------------------------------- combinatorial
@@ -949,7 +1037,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_ada_kernel(
 template <int KIND>
 __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
-    double* psad) {
+    double* psad, double* partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   PPWarpSmem& S = reinterpret_cast<PPWarpSmem*>(smem_raw)[warp];
@@ -1073,8 +1161,8 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     S.res[e][2] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
   }
   __syncwarp();
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (live) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int q = off; q < off + n; ++q) {
 #pragma unroll
       for (int r = 0; r < 3; ++r) acc[r] += S.res[q][r];
@@ -1086,6 +1174,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     }
     store(pmin, pmax, psad, idx, acc);
   }
+  if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
 }
 
 // --------------------------------------------------------------- histogram
@@ -1447,7 +1536,7 @@ CPB_D double pairwise16(const double* w, int n) {
 template <int HB>
 __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     FieldView f, int64_t row_begin, int64_t row_end, int ctiles, double* pmin, double* pmax,
-    double* psad) {
+    double* psad, double* partial) {
   extern __shared__ double sm[];
   constexpr int P = kTabP, SW = kTabSW;
   const int h = HB <= 8 ? HB : f.bins;
@@ -1553,7 +1642,8 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   }
   __syncthreads();
   const int64_t r = r0 + threadIdx.y, c = c0 + 1 + threadIdx.x;
-  if (r >= row_end || c >= f.width - 1) return;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (r < row_end && c < f.width - 1) {
   const int ic = (threadIdx.y + 1) * SW + threadIdx.x + 1;
   const int ip[5] = {ic, ic + 1, ic - SW, ic - 1, ic + SW};  // C E N W S
   const bool fast = RATIO[ip[0]] <= kFastRatio && RATIO[ip[1]] <= kFastRatio &&
@@ -1577,7 +1667,6 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   }
   int kc = 1;
   double pdf = T[K4 + P + ip[0]], nextc = T[K4 + 3 * P + ip[0]];
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
   double x = x0;
   while (x < xend) {
     const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
@@ -1632,8 +1721,9 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     }
     x = dmax(x, xn);
   }
-  const int64_t idx = r * f.width + c;
-  store(pmin, pmax, psad, idx, acc);
+  store(pmin, pmax, psad, r * f.width + c, acc);
+  }
+  if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
 }
 
 }  // namespace
@@ -1658,8 +1748,14 @@ int launch_combinatorial(const cpb_field* fld, int64_t row_begin, int64_t row_en
   return CPB_OK;
 }
 
+int workspace_alloc(void** p, size_t bytes, cudaStream_t st);
+void workspace_free(void* p, cudaStream_t st);
+
+// counts (optional, 3 doubles): the per-type sums of this launch's vertices are
+// ADDED to counts[0..2] (fused into the stencils' epilogue where supported,
+// otherwise a reduction over the written rows)
 int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
-                  double* pmax, double* psad, cudaStream_t st) {
+                  double* pmax, double* psad, cudaStream_t st, double* counts) {
   const FieldView f = make_view(*fld);
   const int64_t rows = row_end - row_begin;
   if (rows <= 0 || f.width < 3) return CPB_OK;
@@ -1676,17 +1772,34 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
   const int64_t cols = f.width - 2, nvert = rows * cols;
   const int64_t pp_blocks = (nvert + kPPWarps * 32 - 1) / (kPPWarps * 32);
   const size_t pp_smem = sizeof(PPWarpSmem) * kPPWarps;
+  // per-block partial sums of the expected counts (freed on every path)
+  struct Partial {
+    double* p = nullptr;
+    int64_t n = 0;
+    cudaStream_t st;
+    ~Partial() { workspace_free(p, st); }
+  } part{nullptr, 0, st};
+  auto want_partial = [&](int64_t nwarps) -> int {  // one partial triple per warp
+    if (!counts) return CPB_OK;
+    part.n = nwarps;
+    return workspace_alloc((void**)&part.p, (size_t)(nwarps + kCountChunks) * 3 * sizeof(double), st);
+  };
+  bool fused_counts = false;  // set by the kernels that write block partials
   switch (f.kind) {
     case CPB_UNIFORM:
       // 3-node pieces are too cheap to amortise the redistribution (measured
       // 18.6 ms per-lane vs 25.4 ms piece-parallel at 16384^2): per-lane by default
       if (pp != 2) {
-        closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
+        if (int rc = want_partial(blocks * (kClosedThreads / 32))) return rc;
+        closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
+        fused_counts = true;
         break;
       }
+      if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
       cudaFuncSetAttribute(closed_pp_kernel<CPB_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
       closed_pp_kernel<CPB_UNIFORM><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
-          f, row_begin, nvert, cols, pmin, pmax, psad);
+          f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
+      fused_counts = true;
       break;
     case CPB_EPANECHNIKOV: {
       if (!pp) {
@@ -1701,9 +1814,11 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
             f, row_begin, nvert, cols, pmin, pmax, psad);
         break;
       }
+      if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
       cudaFuncSetAttribute(closed_pp_kernel<CPB_EPANECHNIKOV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
       closed_pp_kernel<CPB_EPANECHNIKOV><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
-          f, row_begin, nvert, cols, pmin, pmax, psad);
+          f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
+      fused_counts = true;
       break;
     }
     case CPB_HISTOGRAM: {
@@ -1724,9 +1839,11 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
           case 8: kern = closed_hist_tab_kernel<8>; break;
           default: break;
         }
+        if (int rc = want_partial(rtiles * ctiles * (kTabTW * kTabTH / 32))) return rc;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_smem);
         kern<<<(unsigned)(rtiles * ctiles), dim3(kTabTW, kTabTH), tab_smem, st>>>(
-            f, row_begin, row_end, ctiles, pmin, pmax, psad);
+            f, row_begin, row_end, ctiles, pmin, pmax, psad, part.p);
+        fused_counts = true;
         break;
       }
       if (f.bins > kHistSmemMaxBins) {
@@ -1753,6 +1870,19 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       return CPB_EINVAL;
   }
   CPB_CHECK_LAUNCH("closed-form kernel");
+  if (counts) {
+    if (!fused_counts) {  // A/B kernel variants: reduce the written rows instead
+      const int64_t nb = std::min<int64_t>(4096, (nvert + 255) / 256);
+      if (int rc = want_partial(nb * 8)) return rc;
+      rows_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(pmin, pmax, psad, row_begin, cols, f.width,
+                                                         nvert, part.p);
+      CPB_CHECK_LAUNCH("count rows");
+    }
+    double* chunk = part.p + 3 * part.n;
+    counts_reduce_kernel<<<kCountChunks, 256, 0, st>>>(part.p, part.n, chunk);
+    counts_finish_kernel<<<1, 256, 0, st>>>(chunk, kCountChunks, counts);
+    CPB_CHECK_LAUNCH("count finish");
+  }
   return CPB_OK;
 }
 

@@ -311,15 +311,19 @@ def classify_slab(dev, slab: Slab, estimator, channels=("min", "max", "saddle"),
     if out is None:
         out = torch.zeros((3, H, W), dtype=torch.float64, device=dev.device)
     a, b = slab.stencil_rows()
+    # closed form: the per-type sums come out of the stencil kernels' epilogue
+    fused = sums and estimator.method == "closed_form" and set(channels) == {"min", "max", "saddle"}
+    total = torch.zeros(3, dtype=torch.float64, device=dev.device) if fused else None
     if timer:
         timer("classify", True)
     if b > a:
-        run_rows(dev, estimator, channels, a, b, {"min": out[0], "max": out[1], "saddle": out[2]})
+        run_rows(dev, estimator, channels, a, b, {"min": out[0], "max": out[1], "saddle": out[2]},
+                 type_sums=total)
     if timer:
         timer("classify", False)
-    total = None
     if sums:
-        total = out[:, a:b].sum(dim=(1, 2)) if b > a else torch.zeros(3, dtype=torch.float64,
-                                                                        device=dev.device)
+        if not fused:
+            total = out[:, a:b].sum(dim=(1, 2)) if b > a else torch.zeros(3, dtype=torch.float64,
+                                                                            device=dev.device)
         allreduce_sums(total, group)
     return out, total

@@ -82,16 +82,25 @@ def _validate(field: UncertainField, estimator: EstimatorSpec, workers: int, cha
 
 
 def run_rows(dev, estimator: EstimatorSpec, channels, row_begin: int, row_end: int, out: dict,
-             counts=None) -> None:
-    """Enqueue the estimator for local rows [row_begin, row_end) into device planes ``out``."""
+             counts=None, type_sums=None) -> None:
+    """Enqueue the estimator for local rows [row_begin, row_end) into device planes ``out``.
+
+    ``type_sums`` (closed form): a 3-double CUDA tensor the per-type sums of
+    these rows are ADDED to, fused into the stencil kernels' epilogue.
+    """
     lib = _lib.load()
     s = _lib.stream_ptr()
     pm = out["min"] if "min" in channels else None
     pM = out["max"] if "max" in channels else None
     pS = out["saddle"] if "saddle" in channels else None
     if estimator.method == "closed_form":
-        _lib.check(lib.cpb_classify_closed(dev.ref(), row_begin, row_end, _lib.ptr(pm),
-                                           _lib.ptr(pM), _lib.ptr(pS), s))
+        if type_sums is not None:
+            _lib.check(lib.cpb_classify_closed_counts(dev.ref(), row_begin, row_end, _lib.ptr(pm),
+                                                      _lib.ptr(pM), _lib.ptr(pS),
+                                                      type_sums.data_ptr(), s))
+        else:
+            _lib.check(lib.cpb_classify_closed(dev.ref(), row_begin, row_end, _lib.ptr(pm),
+                                               _lib.ptr(pM), _lib.ptr(pS), s))
     elif estimator.method == "monte_carlo":
         seed = int(estimator.seed) & ((1 << 64) - 1)
         _lib.check(lib.cpb_classify_mc(dev.ref(), row_begin, row_end, seed,

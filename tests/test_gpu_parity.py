@@ -550,3 +550,26 @@ def test_row_slabs_on_device_match_single_gpu():
                 got = out[c, a:b].cpu().numpy()
                 assert np.array_equal(got, ref_c.channel(ch)[g0 + a:g0 + b]), (m.kind, ch)
                 assert np.array_equal(outm[c, a:b].cpu().numpy(), ref_m.channel(ch)[g0 + a:g0 + b]), (m.kind, ch)
+
+
+def test_closed_counts_fused_match_plane_sums():
+    """cpb_classify_closed_counts: the per-type sums fused into the stencils equal
+    the sums of the written planes (to rounding) for every model and kernel."""
+    from paper_2407_18015_b200 import _lib
+    from paper_2407_18015_b200.engine import run_rows
+
+    vals = orc.ackley_ensemble(70, 45, 12, noise_amp=0.3, seed=2)
+    for kind, bins in (("uniform", 5), ("epanechnikov", 5), ("histogram", 5), ("histogram", 12),
+                       ("histogram", 30)):
+        field = _fit(vals, kind, bins)
+        dev = field.device_field()
+        out = torch.zeros((3, 45, 70), dtype=torch.float64, device="cuda")
+        sums = torch.zeros(3, dtype=torch.float64, device="cuda")
+        run_rows(dev, cpb.EstimatorSpec(), ("min", "max", "saddle"), 1, 44,
+                 {"min": out[0], "max": out[1], "saddle": out[2]}, type_sums=sums)
+        ref = out[:, 1:44, 1:69].sum(dim=(1, 2))
+        assert torch.allclose(sums, ref, rtol=1e-13, atol=0), (kind, bins, sums, ref)
+        prob = cpb.classify_field(field)
+        assert np.array_equal(out[0].cpu().numpy(), prob.p_min), kind
+    with pytest.raises(ValueError):
+        _lib.check(_lib.load().cpb_classify_closed_counts(dev.ref(), 1, 44, None, None, None, None, 0))
