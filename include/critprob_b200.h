@@ -62,6 +62,13 @@ enum {
   CPB_RNG_PHILOX = 1    /* Philox4x32-10 keyed by (seed, pixel, plane): statistical parity only */
 };
 
+/* cpb_field.flags */
+enum {
+  CPB_FLAG_MIXED = 1 /* closed form: float64 partition / node offsets / accumulation, single-
+                        precision Gauss-Legendre evaluation (north_star bound 1e-6 absolute;
+                        measured in tests/test_gpu_parity.py) */
+};
+
 /* Storage of the support bounds / histogram weights inside a cpb_field. */
 enum {
   CPB_BOUNDS_F32_FITTED = 0, /* lo/hi = raw member min/max (exact in f32); lo==hi pixels are
@@ -94,7 +101,7 @@ typedef struct cpb_field {
   int32_t members;
   int32_t bounds;        /* CPB_BOUNDS_* */
   int32_t weights_mode;  /* CPB_WEIGHTS_* */
-  int32_t reserved;
+  int32_t flags;        /* CPB_FLAG_* */
   int64_t height;        /* local rows (a slab includes its halo rows) */
   int64_t width;
   int64_t row0;          /* global row index of local row 0 (Monte Carlo pixel keys) */

@@ -19,6 +19,7 @@ CH_MIN, CH_MAX, CH_SADDLE = 1, 2, 4
 RNG_CODES = {"splitmix64": 0, "philox": 1}
 BOUNDS_F32_FITTED, BOUNDS_F64 = 0, 1
 WEIGHTS_U8, WEIGHTS_U16, WEIGHTS_F64 = 0, 1, 2
+FLAG_MIXED = 1
 
 c_i32, c_i64, c_u32, c_u64, c_dbl, c_vp = (ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
                                             ctypes.c_uint64, ctypes.c_double, ctypes.c_void_p)
@@ -29,7 +30,7 @@ class CpbField(ctypes.Structure):
 
     _fields_ = [
         ("kind", c_i32), ("bins", c_i32), ("members", c_i32), ("bounds", c_i32),
-        ("weights_mode", c_i32), ("reserved", c_i32),
+        ("weights_mode", c_i32), ("flags", c_i32),
         ("height", c_i64), ("width", c_i64), ("row0", c_i64), ("global_width", c_i64),
         ("plane_stride", c_i64), ("eps_device", c_vp),
         ("eps", c_dbl), ("k", c_dbl),

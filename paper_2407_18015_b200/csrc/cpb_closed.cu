@@ -109,6 +109,32 @@ CPB_D void gl3_sym_sums(const double* Fm, const double* d, double s[4]) {
   s[3] = term(snss, fefw);
 }
 
+// gl3_sym_sums in single precision (the mixed-precision closed form: the
+// partition, node offsets and accumulation stay float64, the per-piece GL3
+// evaluation runs on the FP32 pipes).
+CPB_D void gl3_sym_sums_f(const float* Fm, const float* d, float s[4]) {
+  struct Pair { float p0, pe, po; };
+  auto pair = [](float x0, float dx, float y0, float dy) {
+    Pair r;
+    r.p0 = x0 * y0;
+    r.pe = fmaf(dx, dy, r.p0);
+    r.po = fmaf(x0, dy, y0 * dx);
+    return r;
+  };
+  const float sE = 1.0f - Fm[E_], sN = 1.0f - Fm[N_], sW = 1.0f - Fm[W_], sS = 1.0f - Fm[S_];
+  const Pair sesw = pair(sE, -d[E_], sW, -d[W_]), snss = pair(sN, -d[N_], sS, -d[S_]);
+  const Pair fefw = pair(Fm[E_], d[E_], Fm[W_], d[W_]), fnfs = pair(Fm[N_], d[N_], Fm[S_], d[S_]);
+  const float w1 = (float)GL3::w(1), w0x2 = (float)(2.0 * GL3::w(0));
+  auto term = [&](const Pair& P, const Pair& Q) {
+    const float gs = fmaf(P.po, Q.po, P.pe * Q.pe);
+    return fmaf(w0x2, gs, w1 * (P.p0 * Q.p0));
+  };
+  s[0] = term(sesw, snss);
+  s[1] = term(fefw, fnfs);
+  s[2] = term(sesw, fnfs);
+  s[3] = term(snss, fefw);
+}
+
 CPB_D void store(double* pmin, double* pmax, double* psad, int64_t idx, const double acc[4]) {
   if (pmin) pmin[idx] = acc[0];
   if (pmax) pmax[idx] = acc[1];
@@ -498,6 +524,97 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
     store(pmin, pmax, psad, idx, acc);
   }
   if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
+}
+
+// ------------------------------------------------ uniform, mixed precision
+// CPB_FLAG_MIXED: the five supports are re-centred on lo_C in float64 and the
+// rest -- merge, piece states, GL3 sums -- runs in single precision on the
+// FP32 pipes, with a compensated (Kahan) sum over the pieces.  Absolute error
+// bound 1e-6 (north_star); measured ~1e-7 (tests/test_gpu_parity.py).
+CPB_D void tcswapf(float& a, float& b, int& ta, int& tb) {
+  const bool sw = b < a;
+  const float x = sw ? b : a, y = sw ? a : b;
+  const int u = sw ? tb : ta, v = sw ? ta : tb;
+  a = x; b = y; ta = u; tb = v;
+}
+
+CPB_D void kahan_add(float& sum, float& c, float v) {
+  const float y = v - c;
+  const float t = sum + y;
+  c = (t - sum) - y;
+  sum = t;
+}
+
+CPB_D void uniform_integrals_f(const double* lo, const double* hi, double out[3]) {
+  const double ref = lo[C_];
+  float l[5], h[5], inv[5];
+#pragma unroll
+  for (int p = 0; p < 5; ++p) {
+    l[p] = (float)(lo[p] - ref);
+    h[p] = (float)(hi[p] - ref);
+    inv[p] = 1.0f / (h[p] - l[p]);
+  }
+  float k[8];
+  int t[8];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    k[2 * p - 2] = fminf(fmaxf(l[p], l[C_]), h[C_]);
+    k[2 * p - 1] = fminf(fmaxf(h[p], l[C_]), h[C_]);
+    t[2 * p - 2] = 2 * p - 2;
+    t[2 * p - 1] = 2 * p - 1;
+  }
+  tcswapf(k[0], k[2], t[0], t[2]); tcswapf(k[1], k[3], t[1], t[3]); tcswapf(k[1], k[2], t[1], t[2]);
+  tcswapf(k[4], k[6], t[4], t[6]); tcswapf(k[5], k[7], t[5], t[7]); tcswapf(k[5], k[6], t[5], t[6]);
+  tcswapf(k[0], k[4], t[0], t[4]); tcswapf(k[1], k[5], t[1], t[5]); tcswapf(k[2], k[6], t[2], t[6]);
+  tcswapf(k[3], k[7], t[3], t[7]);
+  tcswapf(k[2], k[4], t[2], t[4]); tcswapf(k[3], k[5], t[3], t[5]);
+  tcswapf(k[1], k[2], t[1], t[2]); tcswapf(k[3], k[4], t[3], t[4]); tcswapf(k[5], k[6], t[5], t[6]);
+  float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f}, cmp[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  float a = l[C_];
+  unsigned cnt = 0;
+  const float tau_x = (float)GL3::x(2);
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const float b = i < 8 ? k[i] : h[C_];
+    if (b > a) {
+      const float half = 0.5f * (b - a), mid = 0.5f * (b + a), tau = half * tau_x;
+      float Fm[5], d[5];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        const unsigned c = (cnt >> (2 * (p - 1))) & 3u;
+        const bool in = c == 1u;
+        Fm[p] = in ? (mid - l[p]) * inv[p] : (c == 2u ? 1.0f : 0.0f);
+        d[p] = in ? tau * inv[p] : 0.0f;
+      }
+      float sp[4];
+      gl3_sym_sums_f(Fm, d, sp);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) kahan_add(acc[r], cmp[r], sp[r] * half);
+      a = b;
+    }
+    if (i < 8) cnt += 1u << (2 * (t[i] >> 1));
+  }
+  out[0] = (double)(acc[0] * inv[C_]);
+  out[1] = (double)(acc[1] * inv[C_]);
+  out[2] = (double)((acc[2] + acc[3]) * inv[C_]);
+}
+
+__global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
+    FieldView f, Window w, double* pmin, double* pmax, double* psad, double* partial) {
+  int64_t idx = 0;
+  const bool live = vertex(f, w, idx);
+  double res[3] = {0.0, 0.0, 0.0};
+  if (live) {
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    double lo[5], hi[5];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+    uniform_integrals_f(lo, hi, res);
+    if (pmin) pmin[idx] = res[0];
+    if (pmax) pmax[idx] = res[1];
+    if (psad) psad[idx] = res[2];
+  }
+  if (partial) warp_partial_sums(res[0], res[1], res[2], partial);
 }
 
 // --------------------------------------------------------- combinatorial
@@ -1756,7 +1873,9 @@ void workspace_free(void* p, cudaStream_t st);
 // otherwise a reduction over the written rows)
 int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
                   double* pmax, double* psad, cudaStream_t st, double* counts) {
-  const FieldView f = make_view(*fld);
+  FieldView f = make_view(*fld);
+  static const int mixed_env = [] { const char* e = getenv("CPB_MIXED"); return e ? atoi(e) : 0; }();
+  if (mixed_env) f.mixed = 1;
   const int64_t rows = row_end - row_begin;
   if (rows <= 0 || f.width < 3) return CPB_OK;
   Window w;
@@ -1791,7 +1910,10 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       // 18.6 ms per-lane vs 25.4 ms piece-parallel at 16384^2): per-lane by default
       if (pp != 2) {
         if (int rc = want_partial(blocks * (kClosedThreads / 32))) return rc;
-        closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
+        if (f.mixed)
+          closed_uniform_f32_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
+        else
+          closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
         fused_counts = true;
         break;
       }

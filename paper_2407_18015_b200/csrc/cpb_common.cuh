@@ -234,6 +234,7 @@ CPB_D double pairwise_sum(const Get& get, int n) {
 // ---------------------------------------------------------------------------
 struct FieldView {
   int kind, bins, members, bounds, wmode;
+  int mixed;        // CPB_FLAG_MIXED: single-precision GL evaluation in the closed form
   int64_t height, width, row0, gwidth;
   int64_t npix;     // height * width
   int64_t wstride;  // elements between histogram bin planes
@@ -257,6 +258,7 @@ inline FieldView make_view(const cpb_field& f) {
   v.eps_dev = f.eps_device;
   v.lo = f.lo; v.hi = f.hi; v.mean = f.mean; v.spread = f.spread; v.weights = f.weights;
   v.wtab = f.weight_table;
+  v.mixed = (f.flags & CPB_FLAG_MIXED) ? 1 : 0;
   return v;
 }
 
