@@ -71,6 +71,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--serial", action="store_true", help="no fit/stencil overlap (one stream)")
+    p.add_argument("--precision", choices=("fp64", "mixed"), default="fp64",
+                   help="closed form: fp64 (reference parity ~1e-15) or mixed (FP32 GL evaluation "
+                        "for uniform / Epanechnikov, stated bound 1e-6)")
     p.add_argument("--fit-priority", choices=("high", "low"), default="high",
                    help="stream priority of the (overlapped) fit relative to the stencils")
     p.add_argument("--concurrent-stencils", action="store_true",
@@ -190,7 +193,7 @@ def run_ours(args):
     ens = cpb.synthetic_rows(slab.row_begin, slab.owned, W, H, M, noise_amp=0.3, seed=0)
     torch.cuda.synchronize()
     out = torch.zeros((3, slab.local_height, W), dtype=torch.float64, device=device)
-    est = cpb.EstimatorSpec()
+    est = cpb.EstimatorSpec(precision=args.precision)
     timer = KernelTimer()
     sums = {}
     overlap = not args.serial
@@ -392,7 +395,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "Mvertices/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f64 (histogram) / mixed f64-f32 (uniform, epanechnikov)",
             "data": "synthetic (device-generated bowl + keyed-splitmix noise, host-reproducible)",
             "config": {"workload": f"config5: {H}x{W} grid, {M} members, closed form, one step = "
                                    f"fit + min/max/saddle for {'+'.join(models)} (bins={bins})",
@@ -411,6 +415,8 @@ def run_ours(args):
 
 
 def cpu_baseline_and_parity(args, models, ens, out_unused, est, slab):
+    # fp64: the reference's own grid-vs-case tolerance; mixed: the north_star's stated bound
+    tol = 1e-12 if est.precision == "fp64" else 1e-6
     """Oracle on rows [r0, r0+6) of the same ensemble (host twin), 1 thread; GPU rows compared."""
     import torch
 
@@ -451,8 +457,8 @@ def cpu_baseline_and_parity(args, models, ens, out_unused, est, slab):
                      f"per model, all {len(models)} models), numpy oracle, 1 thread, fit+classify",
            "seconds": {k: round(v, 3) for k, v in times.items()}}
     parity = {"rows": [r0 + 1, r0 + nr - 1], "input_bit_identical": bit_identical_input,
-              "max_abs_err_vs_oracle": errs, "tolerance": 1e-12,
-              "ok": bit_identical_input and all(e <= 1e-12 for e in errs.values())}
+              "max_abs_err_vs_oracle": errs, "tolerance": tol,
+              "ok": bit_identical_input and all(e <= tol for e in errs.values())}
     return cpu, parity
 
 

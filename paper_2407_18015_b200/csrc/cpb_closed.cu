@@ -607,9 +607,21 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
   if (live) {
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
     double lo[5], hi[5];
+    bool fast = true;
 #pragma unroll
-    for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
-    uniform_integrals_f(lo, hi, res);
+    for (int p = 0; p < 5; ++p) {
+      load_bounds(f, at[p], lo[p], hi[p]);
+      fast &= fabs(lo[p]) + fabs(hi[p]) <= kFastRatio * (hi[p] - lo[p]);
+    }
+    if (fast) {
+      uniform_integrals_f(lo, hi, res);
+    } else {  // tiny supports far from 0 (eps-widened pixels): the fp64 exact mode
+      double acc[4];
+      uniform_integrals(lo, hi, acc);
+      res[0] = acc[0];
+      res[1] = acc[1];
+      res[2] = acc[2] + acc[3];
+    }
     if (pmin) pmin[idx] = res[0];
     if (pmax) pmax[idx] = res[1];
     if (psad) psad[idx] = res[2];
@@ -1149,9 +1161,57 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_epan_ada_kernel(
   }
 }
 
+// Mixed-precision Epanechnikov piece (CPB_FLAG_MIXED): positions re-centred on
+// the centre mean in float64 by the owner lane, the 8-node evaluation in FP32.
+CPB_D float epan_cdf_f(float u) { return fmaf(u, fmaf(-0.25f, u * u, 0.75f), 0.5f); }
+
+CPB_D void integrands_f(const float* F, float g[4]) {
+  const float sE = 1.0f - F[E_], sN = 1.0f - F[N_], sW = 1.0f - F[W_], sS = 1.0f - F[S_];
+  const float sesw = sE * sW, snss = sN * sS;
+  const float fefw = F[E_] * F[W_], fnfs = F[N_] * F[S_];
+  g[0] = sesw * snss;
+  g[1] = fefw * fnfs;
+  g[2] = sesw * fnfs;
+  g[3] = snss * fefw;
+}
+
+CPB_D void epan_piece_f(float a, float b, const float* m, const float* ih, unsigned state,
+                        float s[4]) {
+  const float pdf0 = 0.75f * ih[C_];
+  const float half = 0.5f * (b - a), mid = 0.5f * (b + a);
+  float al[5], be[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    const unsigned c = (state >> (2 * (p - 1))) & 3u;
+    const bool in = c == 1u;
+    be[p] = in ? ih[p] : 0.0f;
+    al[p] = in ? (mid - m[p]) * ih[p] : (c == 2u ? 1.0f : -1.0f);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) s[r] = 0.0f;
+  const float uc0 = (mid - m[C_]) * ih[C_];
+#pragma unroll
+  for (int j = 0; j < GL8::n / 2; ++j) {
+    const float tau = half * (float)GL8::x(7 - j);
+    const float wj = (float)GL8::w(j);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const float t = side ? tau : -tau;
+      const float uc = fmaf(t, ih[C_], uc0);
+      const float wp = wj * (pdf0 * fmaf(-uc, uc, 1.0f));
+      float F[5], g[4];
+#pragma unroll
+      for (int p = 1; p < 5; ++p) F[p] = epan_cdf_f(fmaf(t, be[p], al[p]));
+      integrands_f(F, g);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) s[r] = fmaf(wp, g[r], s[r]);
+    }
+  }
+}
+
 // KIND = CPB_UNIFORM (vertex constants lo[5], hi[5], inv[5]) or
 // CPB_EPANECHNIKOV (m[5], ih[5], lo[1..4], hi[1..4]).
-template <int KIND>
+template <int KIND, bool MX = false>
 __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
     double* psad, double* partial) {
@@ -1164,6 +1224,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   int n = 0;
   double pts[10];
   int tg[8];
+  double mref = 0.0;  // MX: the centre mean, origin of the float coordinates
   if (live) {
     const int64_t r = row_begin + v / cols, c = 1 + v % cols;
     idx = r * f.width + c;
@@ -1186,6 +1247,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
       for (int p = 0; p < 5; ++p) {
         double hw;
         load_epan(f, at[p], m[p], hw);
+        if (p == 0) mref = m[0];
         ih[p] = 1.0 / hw;
         lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
         hi[p] = m[p] + hw;
@@ -1196,10 +1258,13 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
         S.vd[p][lane] = m[p];
         S.vd[5 + p][lane] = ih[p];
       }
+      if (MX) {  // float copies re-centred on the centre mean (fp64 subtraction), rows 10..
+        float* vf = reinterpret_cast<float*>(&S.vd[10][0]);
 #pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        S.vd[9 + p][lane] = lo[p];
-        S.vd[13 + p][lane] = hi[p];
+        for (int p = 0; p < 5; ++p) {
+          vf[p * 32 + lane] = (float)(m[p] - m[C_]);
+          vf[(5 + p) * 32 + lane] = (float)ih[p];
+        }
       }
     }
     S.fast[lane] = fast ? 1 : 0;
@@ -1234,8 +1299,13 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
       if (pts[i + 1] > pts[i]) {
-        S.pa[q] = pts[i];
-        S.pb[q] = pts[i + 1];
+        if (MX && S.fast[lane]) {  // float position in the first word of the slot
+          reinterpret_cast<float*>(&S.pa[q])[0] = (float)(pts[i] - mref);
+          reinterpret_cast<float*>(&S.pb[q])[0] = (float)(pts[i + 1] - mref);
+        } else {
+          S.pa[q] = pts[i];
+          S.pb[q] = pts[i + 1];
+        }
         S.owner[q] = (unsigned char)lane;
         S.state[q] = (unsigned char)cnt;
         ++q;
@@ -1260,13 +1330,30 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
       if (S.fast[o]) uniform_piece<true>(a, b, lo, hi, inv, s, mk);
       else uniform_piece<false>(a, b, lo, hi, inv, s, mk);
     } else {
+      const unsigned st = S.state[e];
+      if (MX && S.fast[o]) {
+        const float* vf = reinterpret_cast<const float*>(&S.vd[10][0]);
+        float mf[5], ihf[5], sf[4];
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+          mf[p] = vf[p * 32 + o];
+          ihf[p] = vf[(5 + p) * 32 + o];
+        }
+        const float fa = reinterpret_cast<const float*>(&S.pa[e])[0];
+        const float fb = reinterpret_cast<const float*>(&S.pb[e])[0];
+        epan_piece_f(fa, fb, mf, ihf, st, sf);
+        const double hf = 0.5 * (double)(fb - fa);
+        S.res[e][0] = (double)sf[0] * hf;
+        S.res[e][1] = (double)sf[1] * hf;
+        S.res[e][2] = (double)(sf[2] + sf[3]) * hf;
+        continue;
+      }
       double m[5], ih[5];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
         m[p] = S.vd[p][o];
         ih[p] = S.vd[5 + p][o];
       }
-      const unsigned st = S.state[e];
       if (S.fast[o]) epan_piece_st<true>(a, b, m, ih, st, s);
       else epan_piece_st<false>(a, b, m, ih, st, s);
       mk[0] = mk[1] = mk[2] = mk[3] = true;
@@ -1873,9 +1960,7 @@ void workspace_free(void* p, cudaStream_t st);
 // otherwise a reduction over the written rows)
 int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
                   double* pmax, double* psad, cudaStream_t st, double* counts) {
-  FieldView f = make_view(*fld);
-  static const int mixed_env = [] { const char* e = getenv("CPB_MIXED"); return e ? atoi(e) : 0; }();
-  if (mixed_env) f.mixed = 1;
+  const FieldView f = make_view(*fld);
   const int64_t rows = row_end - row_begin;
   if (rows <= 0 || f.width < 3) return CPB_OK;
   Window w;
@@ -1937,8 +2022,9 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
         break;
       }
       if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
-      cudaFuncSetAttribute(closed_pp_kernel<CPB_EPANECHNIKOV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
-      closed_pp_kernel<CPB_EPANECHNIKOV><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
+      auto kern = f.mixed ? closed_pp_kernel<CPB_EPANECHNIKOV, true> : closed_pp_kernel<CPB_EPANECHNIKOV, false>;
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
+      kern<<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
           f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
       fused_counts = true;
       break;

@@ -16,6 +16,7 @@ the semianalytical estimator ``cpb_classify_semi`` and the combinatorial
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -25,6 +26,12 @@ from .fields import CHANNELS, ProbabilityField, UncertainField
 
 PATTERNS = ("min", "max", "saddle")
 ESTIMATOR_METHODS = ("closed_form", "monte_carlo", "semianalytical", "combinatorial")
+# closed form: "fp64" (parity with the reference to ~1e-15) or "mixed": float64
+# partition and accumulation, single-precision Gauss-Legendre evaluation for the
+# uniform and Epanechnikov stencils (north_star bound 1e-6 absolute, measured
+# ~1.5e-7); histogram fields stay fp64 (24-bit positions cannot resolve bin
+# edges several bins away to 1e-6)
+PRECISIONS = ("fp64", "mixed")
 COMBINATORIAL_MAX_BINS = 8
 
 
@@ -42,6 +49,7 @@ class EstimatorSpec:
     c: int = 10000
     seed: int = 0
     rng: str = "splitmix64"
+    precision: str = "fp64"
 
     def __post_init__(self) -> None:
         if self.method not in ESTIMATOR_METHODS:
@@ -50,6 +58,8 @@ class EstimatorSpec:
             raise ValueError("sample counts must be positive")
         if self.rng not in _lib.RNG_CODES:
             raise ValueError(f"unknown rng {self.rng!r}")
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r}")
 
 
 def pixel_index(field: UncertainField, row: int, col: int) -> int:
@@ -94,12 +104,17 @@ def run_rows(dev, estimator: EstimatorSpec, channels, row_begin: int, row_end: i
     pM = out["max"] if "max" in channels else None
     pS = out["saddle"] if "saddle" in channels else None
     if estimator.method == "closed_form":
+        st = dev.ref()
+        if estimator.precision == "mixed":
+            st = _lib.CpbField.from_buffer_copy(dev.struct)
+            st.flags |= _lib.FLAG_MIXED
+            st = ctypes.byref(st)
         if type_sums is not None:
-            _lib.check(lib.cpb_classify_closed_counts(dev.ref(), row_begin, row_end, _lib.ptr(pm),
+            _lib.check(lib.cpb_classify_closed_counts(st, row_begin, row_end, _lib.ptr(pm),
                                                       _lib.ptr(pM), _lib.ptr(pS),
                                                       type_sums.data_ptr(), s))
         else:
-            _lib.check(lib.cpb_classify_closed(dev.ref(), row_begin, row_end, _lib.ptr(pm),
+            _lib.check(lib.cpb_classify_closed(st, row_begin, row_end, _lib.ptr(pm),
                                                _lib.ptr(pM), _lib.ptr(pS), s))
     elif estimator.method == "monte_carlo":
         seed = int(estimator.seed) & ((1 << 64) - 1)

@@ -573,3 +573,38 @@ def test_closed_counts_fused_match_plane_sums():
         assert np.array_equal(out[0].cpu().numpy(), prob.p_min), kind
     with pytest.raises(ValueError):
         _lib.check(_lib.load().cpb_classify_closed_counts(dev.ref(), 1, 44, None, None, None, None, 0))
+
+
+def test_closed_mixed_precision_within_stated_bound(golden):
+    """EstimatorSpec(precision="mixed"): FP32 Gauss-Legendre evaluation for the
+    uniform and Epanechnikov stencils within the north_star's 1e-6 absolute
+    bound of the reference (goldens incl. degenerate / far-offset stacks, and a
+    config-2-shaped field); histogram fields stay fp64 (identical results)."""
+    fit, closed = golden["fit"], golden["closed"]
+    mixed = cpb.EstimatorSpec(precision="mixed")
+    worst = 0.0
+    for key in closed:
+        parts = key.split("/")
+        if len(parts) != 4 or parts[3] != "min":
+            continue
+        name, kind, bins = parts[0], parts[1], int(parts[2])
+        field = _fit(fit[f"ens/{name}"], kind, bins)
+        prob = cpb.classify_field(field, mixed)
+        for ch in ("min", "max", "saddle"):
+            err = float(np.max(np.abs(prob.channel(ch) - closed[f"{name}/{kind}/{bins}/{ch}"])))
+            if kind == "histogram":
+                assert err <= CLOSED_TOL, (name, ch, err)
+            else:
+                assert err <= 1e-6, (name, kind, ch, err)
+                worst = max(worst, err)
+    vals = orc.ackley_ensemble(200, 150, 20, noise_amp=0.3, seed=0)
+    for kind in ("uniform", "epanechnikov"):
+        ref = orc.classify(orc.fit(vals, kind), kind)
+        prob = cpb.classify_field(_fit(vals, kind), mixed)
+        for ch in ("min", "max", "saddle"):
+            err = float(np.max(np.abs(prob.channel(ch) - ref[ch])))
+            assert err <= 1e-6, (kind, ch, err)
+            worst = max(worst, err)
+    print("mixed-precision max |error|", worst)
+    with pytest.raises(ValueError):
+        cpb.EstimatorSpec(precision="fp16")
