@@ -371,12 +371,14 @@ def run_ours(args):
                             for (k, w), r in kern.items()},
                 "compute": compute}
     # our kernels per step: range init, fit(s), weight table (histogram),
-    # range->pair, pair->eps per field, one stencil per model
+    # range->pair, pair->eps per field, one stencil per model and (closed form)
+    # the two expected-count reduction kernels per model
     hist = 1 if "histogram" in models else 0
+    per_model_counts = 2 if est.method == "closed_form" else 0
     if fused:
-        launches_per_step = 1 + 1 + hist + 1 + 2 * len(models)
+        launches_per_step = 1 + 1 + hist + 1 + (2 + per_model_counts) * len(models)
     else:
-        launches_per_step = sum(5 + (1 if k == "histogram" else 0) for k in models)
+        launches_per_step = sum(5 + per_model_counts + (1 if k == "histogram" else 0) for k in models)
 
     # ---- parity spot-check + CPU baseline (rank 0, N = 1)
     cpu = None
