@@ -485,7 +485,15 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
         (s = pair[i].alloc(2 * sizeof(double), s0)) || (s = sens[i].alloc((size_t)height, s0)) ||
         (s = out[i].alloc(3 * plane * sizeof(double), s0)))
       return s;
-    e = cudaMemsetAsync(out[i].p, 0, 3 * plane * sizeof(double), s0);
+    // the stencils write every interior vertex; only the border columns of the
+    // copied rows need zeros (two strided columns per plane, not 3 x H x W)
+    for (int c = 0; c < 3 && e == cudaSuccess; ++c) {
+      double* base = (double*)out[i].p + c * plane;
+      e = cudaMemset2DAsync(base, width * sizeof(double), 0, sizeof(double), (size_t)height, s0);
+      if (e == cudaSuccess)
+        e = cudaMemset2DAsync(base + width - 1, width * sizeof(double), 0, sizeof(double),
+                              (size_t)height, s0);
+    }
     if (e != cudaSuccess) return cuda_status(e, "memset");
     cpb_field& f = fm[i];
     f = cpb_field{};
@@ -625,6 +633,23 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     }
   }
   const double t_enqueued = host_ms();
+  // host work while the device pipeline runs: the border rows of the outputs
+  // (never copied back; zero like the reference's invalid border) and the mask
+  for (int i = 0; i < nm; ++i)
+    for (int c = 0; c < 3; ++c)
+      if (double* dst = h_out ? h_out[3 * i + c] : nullptr) {
+        memset(dst, 0, (size_t)width * sizeof(double));
+        memset(dst + (size_t)(height - 1) * width, 0, (size_t)width * sizeof(double));
+      }
+  if (h_valid) {
+    for (int64_t r = 0; r < height; ++r) {
+      uint8_t* row = h_valid + r * width;
+      const uint8_t inner = (r > 0 && r < height - 1) ? 1 : 0;
+      memset(row, inner, (size_t)width);
+      row[0] = 0;
+      row[width - 1] = 0;
+    }
+  }
   // exactness: rows stencilled with a provisional eps are redone where some
   // pixel's result depends on eps (degenerate / clamped pixels; normally none)
   e = cudaStreamSynchronize(ss.s[0]);
@@ -662,15 +687,6 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
         if ((s = copy_rows(i, v, w))) return s;
         v = w;
       }
-    }
-  }
-  if (h_valid) {
-    for (int64_t r = 0; r < height; ++r) {
-      uint8_t* row = h_valid + r * width;
-      const uint8_t inner = (r > 0 && r < height - 1) ? 1 : 0;
-      memset(row, inner, (size_t)width);
-      row[0] = 0;
-      row[width - 1] = 0;
     }
   }
   e = cudaStreamSynchronize(scls);

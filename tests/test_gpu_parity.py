@@ -362,8 +362,8 @@ def test_run_host_models_matches_oracle():
     vals = np.ascontiguousarray(orc.ackley_ensemble(37, 4099, 6, noise_amp=0.3, seed=3))
     M, H, W = vals.shape
     models = [("uniform", 5), ("epanechnikov", 5), ("histogram", 4)]
-    outs = [np.zeros((H, W)) for _ in range(3 * len(models))]
-    valid = np.zeros((H, W), dtype=np.uint8)
+    outs = [np.full((H, W), np.nan) for _ in range(3 * len(models))]  # every element is written
+    valid = np.full((H, W), 7, dtype=np.uint8)
     kinds = (ctypes.c_int32 * 3)(*[_lib.KIND_CODES[k] for k, _ in models])
     bins = (ctypes.c_int32 * 3)(*[b for _, b in models])
     ks = (ctypes.c_double * 3)(*[float(cpb.ModelSpec(k).k) for k, _ in models])
@@ -376,7 +376,7 @@ def test_run_host_models_matches_oracle():
         for c, ch in enumerate(("min", "max", "saddle")):
             assert np.max(np.abs(outs[3 * i + c] - ref[ch])) <= CLOSED_TOL, (kind, ch)
     # single-model entry point, Monte Carlo
-    o = [np.zeros((H, W)) for _ in range(3)]
+    o = [np.full((H, W), np.nan) for _ in range(3)]
     _lib.check(lib.cpb_run_host(vals.ctypes.data, M, H, W, 0, 5, 1.0, 1, 11, 300, 7,
                                 o[0].ctypes.data, o[1].ctypes.data, o[2].ctypes.data, None))
     ref = orc.classify(orc.fit(vals, "uniform"), "uniform", method="monte_carlo", n_samples=300,
@@ -435,7 +435,7 @@ def test_run_host_streaming_eps_fixup():
     vals[2, 280, 11] = 1000.0     # the last chunk widens the global range, hence eps
     vals = np.ascontiguousarray(vals)
     models = [("uniform", 5), ("epanechnikov", 5), ("histogram", 3)]
-    outs = [np.zeros((H, W)) for _ in range(9)]
+    outs = [np.full((H, W), np.nan) for _ in range(9)]  # the library must write every element
     kinds = (ctypes.c_int32 * 3)(*[_lib.KIND_CODES[k] for k, _ in models])
     bins = (ctypes.c_int32 * 3)(*[b for _, b in models])
     ks = (ctypes.c_double * 3)(*[float(cpb.ModelSpec(k).k) for k, _ in models])
