@@ -11,9 +11,10 @@
 // splitmix64 stream each draw is the reference's (seed, pixel, plane, i)
 // uniform and the inverse CDFs repeat numpy's float64 operations with
 // explicit round-to-nearest intrinsics, so uniform and histogram counts are
-// bit-identical to the reference; Epanechnikov (asin/sin) and Gaussian
-// (log1p/cos) draws can differ from glibc by an ulp, which flips a strict
-// comparison only on an exact tie.
+// bit-identical to the reference; Epanechnikov draws (the cubic's root by a
+// float guess + one float64 Halley step, cpb_sample.cuh) and Gaussian draws
+// (log1p/cos) can differ from glibc's by an ulp or two, which flips a strict
+// comparison only on a tie within that distance (never observed).
 #include "cpb_common.cuh"
 #include "cpb_sample.cuh"
 

@@ -16,6 +16,22 @@ struct Sampler {
   const double* cum;// histogram: h+1 prefix sums, cum[h] = 1 (smem)
 };
 
+// Root t in [-1, 1] of t^3 - 3t + 2y = 0, i.e. the reference's
+// 2 sin(asin(y) / 3) (distributions.py:64-70, y = 2u - 1), without float64
+// transcendentals: a single-precision guess (error ~1e-6) and one Halley step
+// in float64 (cubic convergence, ~1e-18), so the draw agrees with the
+// reference's libm evaluation to an ulp or two -- a strict comparison can only
+// flip on a tie within that ulp.  Near |y| = 1 the root is double and the
+// Halley step loses its rate, so there the reference formula is evaluated.
+CPB_D double epan_root(double y) {
+  if (fabs(y) > 0.999) return __dmul_rn(2.0, sin(__ddiv_rn(asin(y), 3.0)));
+  const double t = (double)(2.0f * __sinf(asinf((float)y) * (1.0f / 3.0f)));
+  const double t2 = t * t;
+  const double g = fma(t, t2 - 3.0, 2.0 * y);
+  const double gp = 3.0 * (t2 - 1.0);
+  return t - (2.0 * g * gp) / fma(2.0 * gp, gp, -g * 6.0 * t);
+}
+
 template <int KIND>
 CPB_D double draw(const Sampler& s, double u, double u2, int h) {
   if (KIND == CPB_UNIFORM) {  // (1 - u) lo + u hi  (distributions.py:60-61)
@@ -23,7 +39,7 @@ CPB_D double draw(const Sampler& s, double u, double u2, int h) {
   } else if (KIND == CPB_EPANECHNIKOV) {  // distributions.py:64-70
     if (u == 0.0) return __dsub_rn(s.a, s.b);
     if (u == 1.0) return __dadd_rn(s.a, s.b);
-    const double root = __dmul_rn(2.0, sin(__ddiv_rn(asin(__dsub_rn(__dmul_rn(2.0, u), 1.0)), 3.0)));
+    const double root = epan_root(__dsub_rn(__dmul_rn(2.0, u), 1.0));
     return __dadd_rn(s.a, __dmul_rn(s.b, root));
   } else if (KIND == CPB_GAUSSIAN) {  // Box-Muller, engine.py:638-640
     const double r = __dsqrt_rn(__dmul_rn(-2.0, log1p(-u)));
