@@ -19,7 +19,7 @@ def golden():
     import numpy as np
 
     return {name: dict(np.load(os.path.join(GOLDEN, name + ".npz")))
-            for name in ("fit", "closed", "mc", "rng", "semi", "comb", "io", "cases")}
+            for name in ("fit", "closed", "mc", "rng", "semi", "comb", "io", "cases", "synth")}
 
 # small host-path chunks so the GPU tests exercise cpb_run_host's chunked
 # upload and chunk views (the library reads this once, at first use)

@@ -273,6 +273,13 @@ def main() -> None:
         io_fx["prob/valid"] = prob.valid
     np.savez_compressed(os.path.join(HERE, "io.npz"), **io_fx)
     np.savez_compressed(os.path.join(HERE, "cases.npz"), **case_fixtures())
+    # synthetic generators used by the acceptance gates (synth.py:54-121)
+    from critprob.synth import gaussian_mixture_ensemble
+
+    mix, peaks, outliers = gaussian_mixture_ensemble(32, 32, true_members=6, outlier_members=3, seed=4)
+    np.savez_compressed(os.path.join(HERE, "synth.npz"), mixture=mix.values,
+                        peaks=np.array(peaks), outlier_peaks=np.array(outliers),
+                        ackley=ackley_ensemble(20, 12, members=5, noise_amp=0.3, seed=7).values)
 
     np.savez_compressed(os.path.join(HERE, "fit.npz"), **fit)
     np.savez_compressed(os.path.join(HERE, "closed.npz"), **closed)
@@ -280,7 +287,7 @@ def main() -> None:
     np.savez_compressed(os.path.join(HERE, "rng.npz"), **rng_fx)
     np.savez_compressed(os.path.join(HERE, "semi.npz"), **semi)
     np.savez_compressed(os.path.join(HERE, "comb.npz"), **comb)
-    for f in ("fit", "closed", "mc", "rng", "semi", "comb", "io", "cases"):
+    for f in ("fit", "closed", "mc", "rng", "semi", "comb", "io", "cases", "synth"):
         print(f, os.path.getsize(os.path.join(HERE, f + ".npz")), "bytes")
 
 

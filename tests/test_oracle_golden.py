@@ -149,3 +149,13 @@ def test_semianalytical_bitexact(golden):
             assert np.array_equal(got[ch], semi[f"{name}/{kind}/{bins}/{ch}"]), (key, ch)
         seen += 1
     assert seen >= 6
+
+
+def test_synthetic_generators_match_reference(golden):
+    """The oracle's ackley_ensemble and gaussian_mixture_ensemble (synth.py:54-121)
+    reproduce the reference's bytes (used to build the acceptance-gate inputs)."""
+    g = golden["synth"]
+    vals, peaks, outliers = orc.gaussian_mixture_ensemble(32, 32, 6, 3, 4)
+    assert np.array_equal(vals, g["mixture"])
+    assert [tuple(p) for p in g["peaks"]] == peaks and [tuple(p) for p in g["outlier_peaks"]] == outliers
+    assert np.array_equal(orc.ackley_ensemble(20, 12, 5, noise_amp=0.3, seed=7), g["ackley"])
