@@ -362,8 +362,22 @@ def _run(cases, fn, pixels=None) -> np.ndarray:
 
 # ------------------------------------------------------------ batch API
 def closed_form_triples(cases) -> np.ndarray:
-    """closed_form_triple of every case: (n, 3) float64."""
-    return _run(_cases(cases), lambda b, _: b.closed())
+    """closed_form_triple of every case: (n, 3) float64.
+
+    As in the reference (engine.py:139-142, 177-178) p_max is the minimum
+    probability of the NEGATED case, so local_max_prob(c) == local_min_prob(
+    c.negate()) holds bit for bit; case objects and their negations go to the
+    device as one batch.  (A prebuilt CaseBatch takes p_max from the direct
+    product-of-CDFs integral of the same walk instead.)
+    """
+    cases = _cases(cases)
+    if isinstance(cases, CaseBatch):
+        return cases.closed()
+    n = len(cases)
+    both = _run(list(cases) + [c.negate() for c in cases], lambda b, _: b.closed())
+    out = both[:n].copy()
+    out[:, 1] = both[n:, 0]
+    return out
 
 
 def mc_all_patterns_batch(cases, n: int, seed: int = 0, pixels=None) -> np.ndarray:
@@ -451,20 +465,21 @@ def case_at(field, row: int, col: int) -> NeighborhoodCase:
     height, width = field.shape
     if not (1 <= row < height - 1 and 1 <= col < width - 1):
         raise ValueError("neighborhood requires an interior pixel")
+    d = field.dist_at
+    return NeighborhoodCase(d(row, col), (d(row, col + 1), d(row - 1, col), d(row, col - 1), d(row + 1, col)))
+
+
+def dist_at(field, row: int, col: int):
+    """The pixel's distribution from the stored parameters (UncertainField.dist_at, fields.py:109-121)."""
     p = field.params
     kind = field.model.kind
-
-    def dist_at(r, c):  # UncertainField.dist_at, fields.py:109-121
-        if kind == "uniform":
-            return uniform(p["lo"][r, c], p["hi"][r, c])
-        if kind == "epanechnikov":
-            return epanechnikov(p["mean"][r, c], p["halfwidth"][r, c])
-        if kind == "histogram":
-            return histogram(p["lo"][r, c], p["hi"][r, c], p["weights"][r, c])
-        return GaussianSampler(float(p["mean"][r, c]), float(p["stddev"][r, c]))
-
-    return NeighborhoodCase(dist_at(row, col), (dist_at(row, col + 1), dist_at(row - 1, col),
-                                                dist_at(row, col - 1), dist_at(row + 1, col)))
+    if kind == "uniform":
+        return uniform(p["lo"][row, col], p["hi"][row, col])
+    if kind == "epanechnikov":
+        return epanechnikov(p["mean"][row, col], p["halfwidth"][row, col])
+    if kind == "histogram":
+        return histogram(p["lo"][row, col], p["hi"][row, col], p["weights"][row, col])
+    return GaussianSampler(float(p["mean"][row, col]), float(p["stddev"][row, col]))
 
 
 # ------------------------------------------------------ random cases / fuzz

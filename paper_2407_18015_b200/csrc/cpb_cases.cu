@@ -149,12 +149,32 @@ CPB_D void case_integrands(const double* F, int k, double g[4]) {
   g[3] = (sN * sS) * (F[1] * F[3]);
 }
 
+// Integrand values at x: g[r] = pdf_C(x) * factors_r(x) when WITH_PDF, else
+// the factors only (a piecewise-constant centre density is applied per piece).
+template <bool WITH_PDF>
+CPB_D void node_values(Walk* d, int P, double x, double g[4]) {
+  double F[kMaxPos];
+  for (int p = 1; p < P; ++p) F[p] = walk_cdf(d[p], x);
+  case_integrands(F, P - 1, g);
+  if (WITH_PDF) {
+    const double pdf = walk_pdf(d[0], x);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) g[r] *= pdf;
+  }
+}
+
+// GL sums over symmetric node pairs: s = w_0 g(mid) [odd n] + sum_j w_j (g(mid - t_j)
+// + g(mid + t_j)).  For a constant integrand this is exactly 2 g (the pair
+// weights of leggauss(3) and leggauss(8) add to exactly 2 in this order), so
+// certain / impossible patterns come out as exactly 1 and 0, as the
+// reference's exact polynomial integration gives them (test_engine.py:114-143).
 template <class GL>
 CPB_D void walk_integrals(Walk* d, int P, double acc[4]) {
   for (int r = 0; r < 4; ++r) acc[r] = 0.0;
   const double hiC = d[0].hi;
   double x0 = d[0].lo;
   for (int p = 0; p < P; ++p) pass_through(d[p], x0);
+  const bool pdf_const = d[0].kind != CPB_EPANECHNIKOV;
   int guard = 0;
   while (x0 < hiC && guard++ < 1 << 20) {
     double x1 = hiC;
@@ -163,18 +183,30 @@ CPB_D void walk_integrals(Walk* d, int P, double acc[4]) {
     if (x1 > x0) {
       const double half = 0.5 * (x1 - x0), mid = 0.5 * (x1 + x0);
       double s[4] = {0.0, 0.0, 0.0, 0.0};
+      if (GL::n % 2 == 1) {  // centre node
+        double g[4];
+        if (pdf_const) node_values<false>(d, P, mid, g);
+        else node_values<true>(d, P, mid, g);
 #pragma unroll
-      for (int q = 0; q < GL::n; ++q) {
-        const double x = mid + half * GL::x(q);
-        double F[kMaxPos], g[4];
-        for (int p = 1; p < P; ++p) F[p] = walk_cdf(d[p], x);
-        case_integrands(F, P - 1, g);
-        const double wq = GL::w(q) * walk_pdf(d[0], x);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = fma(wq, g[r], s[r]);
+        for (int r = 0; r < 4; ++r) s[r] = GL::w(GL::n / 2) * g[r];
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] = fma(half, s[r], acc[r]);
+      for (int j = 0; j < GL::n / 2; ++j) {
+        const double t = half * GL::x(GL::n - 1 - j);  // positive node
+        double gm[4], gp[4];
+        if (pdf_const) {
+          node_values<false>(d, P, mid - t, gm);
+          node_values<false>(d, P, mid + t, gp);
+        } else {
+          node_values<true>(d, P, mid - t, gm);
+          node_values<true>(d, P, mid + t, gp);
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) s[r] = fma(GL::w(GL::n - 1 - j), gm[r] + gp[r], s[r]);
+      }
+      const double scale = pdf_const ? half * walk_pdf(d[0], mid) : half;
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = fma(scale, s[r], acc[r]);
     } else {
       x1 = x0;
     }

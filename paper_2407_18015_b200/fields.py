@@ -308,6 +308,12 @@ class UncertainField:
         dev = fit_device(vals, model)
         return cls(model, _device_field=dev)
 
+    def dist_at(self, row: int, col: int):
+        """Materialize the pixel's distribution (fields.py:109-121) as a per-case object."""
+        from .cases import dist_at
+
+        return dist_at(self, row, col)
+
     @classmethod
     def from_ensemble_models(cls, stack: EnsembleStack, models) -> list:
         """``[from_ensemble(stack, m) for m in models]`` in one pass over the
