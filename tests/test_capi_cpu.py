@@ -69,3 +69,27 @@ def test_no_oracle_on_product_path():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", src, re.M), f
+
+
+def test_header_compiles_as_c_and_links(lib, tmp_path):
+    """A plain C99 program includes the header, links
+    libcritprob_b200.so and calls its host-only entry points."""
+    import shutil
+    import subprocess
+
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "abi.c"
+    src.write_text(
+        '#include <stdio.h>\n#include "critprob_b200.h"\n'
+        "int main(void) {\n"
+        "  cpb_case_batch b = {0};\n  cpb_field f = {0};\n  (void)b; (void)f;\n"
+        '  printf("%d %.17g %.17g\\n", cpb_abi_version(), cpb_epsilon(0.0, 10.0), cpb_epsilon(2.0, 2.0));\n'
+        "  return cpb_abi_version() == CPB_ABI_VERSION ? 0 : 1;\n}\n")
+    libdir = os.path.join(ROOT, "paper_2407_18015_b200")
+    exe = tmp_path / "abi"
+    subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                    "-L", libdir, "-lcritprob_b200", "-Wl,-rpath," + libdir, "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert out[0] == "1" and float(out[1]) == 1e-8 and float(out[2]) == 1e-12
