@@ -430,11 +430,13 @@ __global__ void __launch_bounds__(kCombThreads) cases_semi_kernel(Batch B, uint6
   const uint64_t px = pixels ? pixels[c] : (uint64_t)c;
   const uint64_t key = plane_key(pixel_key(seed, px), 0);
   double smin = 0.0, smax = 0.0, ssad = 0.0;
+  double ib[kMaxPos];
+  for (int p = 0; p < P; ++p) ib[p] = 1.0 / pt[p].s.b;
   for (int64_t i = threadIdx.x; hist && i < cnt; i += kCombThreads) {
     const double x = draw<CPB_HISTOGRAM>(sc, stream_u01(key, (uint64_t)i), 0.0, pt[0].h);
     double F[kMaxPos];
     for (int p = 1; p < P; ++p)
-      F[p] = hist_cdf_at(pt[p].s.wn, pt[p].s.cum, pt[p].s.a, pt[p].s.b, pt[p].h, x);
+      F[p] = hist_cdf_fast(pt[p].s.wn, pt[p].s.cum, pt[p].s.a, pt[p].s.b, ib[p], pt[p].h, x);
     if (P == 3) {
       smin = __dadd_rn(smin, __dmul_rn(__dsub_rn(1.0, F[1]), __dsub_rn(1.0, F[2])));
       smax = __dadd_rn(smax, __dmul_rn(F[1], F[2]));

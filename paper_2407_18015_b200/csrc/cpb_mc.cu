@@ -161,13 +161,14 @@ __global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs
     const int64_t r = a.row_begin + v / a.cols, c = 1 + v % a.cols;
     const int64_t idx = r * f.width + c;
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
-    double lo[5], binw[5];
+    double lo[5], binw[5], ibinw[5];
 #pragma unroll
     for (int p = 0; p < 5; ++p) {
       double l, hh;
       const bool deg = load_bounds(f, at[p], l, hh);
       lo[p] = l;
       binw[p] = __ddiv_rn(__dsub_rn(hh, l), (double)h);
+      ibinw[p] = 1.0 / binw[p];
       if (lane == p) {
         const int dbin = deg ? degenerate_bin((double)__ldg(static_cast<const float*>(f.lo) + at[p]), l, hh, h) : 0;
         const double total = pairwise_sum([&](int b) { return load_weight(f, at[p], b, deg, dbin); }, h);
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs
       double F[5];
 #pragma unroll
       for (int p = 1; p < 5; ++p)
-        F[p] = hist_cdf_at(my_tab + p * tab, my_tab + p * tab + h, lo[p], binw[p], h, x);
+        F[p] = hist_cdf_fast(my_tab + p * tab, my_tab + p * tab + h, lo[p], binw[p], ibinw[p], h, x);
       const double e = F[1], nn = F[2], w = F[3], s = F[4];
       smin = __dadd_rn(smin, __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), __dsub_rn(1.0, nn)),
                                                  __dsub_rn(1.0, w)), __dsub_rn(1.0, s)));

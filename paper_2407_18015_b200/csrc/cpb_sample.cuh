@@ -68,4 +68,18 @@ CPB_D double hist_cdf_at(const double* wn, const double* cum, double lo, double 
   return fmin(fmax(v, 0.0), 1.0);
 }
 
+// hist_cdf_at with the two divisions by binw replaced by a multiplication
+// with ibinw = 1 / binw (semianalytical estimators, whose tolerance is 1e-13:
+// the CDF is continuous, so a bin index off by one where (x - lo) / binw
+// rounds across an integer changes the value only by rounding, and the
+// quotient itself by an ulp).
+CPB_D double hist_cdf_fast(const double* wn, const double* cum, double lo, double binw,
+                           double ibinw, int h, double x) {
+  const double t = floor((x - lo) * ibinw);
+  const int j = (int)fmax(0.0, fmin(t, (double)(h - 1)));
+  const double frac = (x - fma(binw, (double)j, lo)) * ibinw;
+  const double v = fma(wn[j], frac, cum[j]);
+  return fmin(fmax(v, 0.0), 1.0);
+}
+
 }  // namespace cpb
