@@ -1856,21 +1856,22 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   constexpr int K4 = 4 * P;
   const double x0 = T[3 * P + ip[0]];                  // lo_C (NX of state 0)
   const double xend = T[(size_t)h * K4 + 3 * P + ip[0]];  // hi_C (NX of state h)
-  int kp[5];
+  // each list is a pointer to its current state's table column; advancing
+  // is one predicated add of the state stride
+  const double* tp[5];
   double cc_[5], ss[5], ee[5], nx[5];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
-    int k = 0;
-    while (T[k * K4 + 3 * P + ip[p]] <= x0) ++k;
-    kp[p] = k;
-    const double* t = T + k * K4 + ip[p];
+    const double* t = T + ip[p];
+    while (t[3 * P] <= x0) t += K4;
+    tp[p] = t;
     cc_[p] = t[0];
     ss[p] = t[P];
     ee[p] = t[2 * P];
     nx[p] = t[3 * P];
   }
-  int kc = 1;
-  double pdf = T[K4 + P + ip[0]], nextc = T[K4 + 3 * P + ip[0]];
+  const double* tcp = T + K4 + ip[0];
+  double pdf = tcp[P], nextc = tcp[3 * P];
   double x = x0;
   while (x < xend) {
     const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
@@ -1908,22 +1909,18 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = fma(s[q], scale, acc[q]);
     // advance every list whose next edge is xn
-    kc += nextc == xn ? 1 : 0;
-    {
-      const double* t = T + kc * K4 + ip[0];
-      pdf = t[P];
-      nextc = t[3 * P];
-    }
+    tcp += nextc == xn ? K4 : 0;
+    pdf = tcp[P];
+    nextc = tcp[3 * P];
 #pragma unroll
     for (int p = 1; p < 5; ++p) {
-      kp[p] += nx[p] == xn ? 1 : 0;
-      const double* t = T + kp[p] * K4 + ip[p];
-      cc_[p] = t[0];
-      ss[p] = t[P];
-      ee[p] = t[2 * P];
-      nx[p] = t[3 * P];
+      tp[p] += nx[p] == xn ? K4 : 0;
+      cc_[p] = tp[p][0];
+      ss[p] = tp[p][P];
+      ee[p] = tp[p][2 * P];
+      nx[p] = tp[p][3 * P];
     }
-    x = dmax(x, xn);
+    x = xn;  // every next edge lies beyond x, so the partition only moves forward
   }
   store(pmin, pmax, psad, r * f.width + c, acc);
   }
