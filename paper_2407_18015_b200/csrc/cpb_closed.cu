@@ -1741,10 +1741,12 @@ template <int HB>
 __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     FieldView f, int64_t row_begin, int64_t row_end, int ctiles, double* pmin, double* pmax,
     double* psad, double* partial) {
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   constexpr int P = kTabP, SW = kTabSW;
   const int h = HB <= 8 ? HB : f.bins;
-  double* T = sm;                          // [(h + 2) states][4 fields][P pixels]
+  // [(h + 2) states][2 pairs][P pixels] of double2: (CUM, SL) then (EV, NX), so
+  // a list advance is two 16-byte loads (conflict-free: 8 lanes x 16 B)
+  double* T = sm;
   double* RATIO = sm + (size_t)(h + 2) * 4 * P;  // (|lo| + |hi|) / binw, fast-mode test
   const int64_t r0 = row_begin + (int64_t)(blockIdx.x / ctiles) * kTabTH;
   const int64_t c0 = (int64_t)(blockIdx.x % ctiles) * kTabTW;  // staged cols [c0, c0 + SW)
@@ -1755,22 +1757,22 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   auto build = [&](int i, double lo, double hi, const double* wv) {
     const double it = 1.0 / (HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
-    T[0 * P + i] = 0.0; T[1 * P + i] = 0.0; T[2 * P + i] = 0.0; T[3 * P + i] = lo;
+    T[2 * i] = 0.0; T[2 * i + 1] = 0.0; T[2 * P + 2 * i] = 0.0; T[2 * P + 2 * i + 1] = lo;
     double cum = 0.0;
 #pragma unroll
     for (int b = 0; b < HB; ++b) {
       if (b < h) {
         const double wn = wv[b] * it;
-        double* t = T + (size_t)(b + 1) * 4 * P + i;
+        double* t = T + (size_t)(b + 1) * 4 * P + 2 * i;
         t[0] = cum;
-        t[P] = wn * ibinw;
+        t[1] = wn * ibinw;
         t[2 * P] = fma(binw, (double)b, lo);
-        t[3 * P] = b + 1 < h ? fma(width, (double)(b + 1) / dh, lo) : hi;
+        t[2 * P + 1] = b + 1 < h ? fma(width, (double)(b + 1) / dh, lo) : hi;
         cum += wn;
       }
     }
-    double* t = T + (size_t)(h + 1) * 4 * P + i;
-    t[0] = 1.0; t[P] = 0.0; t[2 * P] = 0.0; t[3 * P] = inf;
+    double* t = T + (size_t)(h + 1) * 4 * P + 2 * i;
+    t[0] = 1.0; t[1] = 0.0; t[2 * P] = 0.0; t[2 * P + 1] = inf;
     RATIO[i] = (fabs(lo) + fabs(hi)) * ibinw;
   };
   constexpr int NT = kTabTW * kTabTH, NPT = (P + NT - 1) / NT;
@@ -1854,24 +1856,26 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
                     RATIO[ip[2]] <= kFastRatio && RATIO[ip[3]] <= kFastRatio &&
                     RATIO[ip[4]] <= kFastRatio;
   constexpr int K4 = 4 * P;
-  const double x0 = T[3 * P + ip[0]];                  // lo_C (NX of state 0)
-  const double xend = T[(size_t)h * K4 + 3 * P + ip[0]];  // hi_C (NX of state h)
+  const double x0 = T[2 * P + 2 * ip[0] + 1];                     // lo_C (NX of state 0)
+  const double xend = T[(size_t)h * K4 + 2 * P + 2 * ip[0] + 1];  // hi_C (NX of state h)
   // each list is a pointer to its current state's table column; advancing
   // is one predicated add of the state stride
   const double* tp[5];
   double cc_[5], ss[5], ee[5], nx[5];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
-    const double* t = T + ip[p];
-    while (t[3 * P] <= x0) t += K4;
+    const double* t = T + 2 * ip[p];
+    while (t[2 * P + 1] <= x0) t += K4;
     tp[p] = t;
-    cc_[p] = t[0];
-    ss[p] = t[P];
-    ee[p] = t[2 * P];
-    nx[p] = t[3 * P];
+    const double2 a = *reinterpret_cast<const double2*>(t);
+    const double2 b = *reinterpret_cast<const double2*>(t + 2 * P);
+    cc_[p] = a.x;
+    ss[p] = a.y;
+    ee[p] = b.x;
+    nx[p] = b.y;
   }
-  const double* tcp = T + K4 + ip[0];
-  double pdf = tcp[P], nextc = tcp[3 * P];
+  const double* tcp = T + K4 + 2 * ip[0];
+  double pdf = tcp[1], nextc = tcp[2 * P + 1];
   double x = x0;
   while (x < xend) {
     const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
@@ -1910,15 +1914,17 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     for (int q = 0; q < 4; ++q) acc[q] = fma(s[q], scale, acc[q]);
     // advance every list whose next edge is xn
     tcp += nextc == xn ? K4 : 0;
-    pdf = tcp[P];
-    nextc = tcp[3 * P];
+    pdf = tcp[1];
+    nextc = tcp[2 * P + 1];
 #pragma unroll
     for (int p = 1; p < 5; ++p) {
       tp[p] += nx[p] == xn ? K4 : 0;
-      cc_[p] = tp[p][0];
-      ss[p] = tp[p][P];
-      ee[p] = tp[p][2 * P];
-      nx[p] = tp[p][3 * P];
+      const double2 a = *reinterpret_cast<const double2*>(tp[p]);
+      const double2 b = *reinterpret_cast<const double2*>(tp[p] + 2 * P);
+      cc_[p] = a.x;
+      ss[p] = a.y;
+      ee[p] = b.x;
+      nx[p] = b.y;
     }
     x = xn;  // every next edge lies beyond x, so the partition only moves forward
   }
