@@ -31,12 +31,33 @@ int cuda_status(cudaError_t e, const char* what);
 // (piecewise.py:29-31); 3 nodes for uniform/histogram, 8 for epanechnikov
 // (engine.py:600-601).
 // ---------------------------------------------------------------------------
+// Device code reads the nodes / weights from constant memory, so a DFMA takes
+// them as a c[bank][offset] operand instead of materialising each 64-bit
+// immediate with two UMOVs per use inside the piece loops.
+__constant__ double c_gl3[6] = {-0x1.8c97ef43f7248p-1, 0.0, 0x1.8c97ef43f7248p-1,
+                                0x1.1c71c71c71c73p-1, 0x1.c71c71c71c71cp-1, 0x1.1c71c71c71c73p-1};
+__constant__ double c_gl8[16] = {
+    -0x1.ebab1cb0acc66p-1, -0x1.97e4ab249f41ep-1, -0x1.0d129583284b4p-1, -0x1.77ac94f3c7344p-3,
+    0x1.77ac94f3c7344p-3,  0x1.0d129583284b4p-1,  0x1.97e4ab249f41ep-1,  0x1.ebab1cb0acc66p-1,
+    0x1.9ea1d04ca03aep-4,  0x1.c76fb531d2b94p-3,  0x1.413c50a25560ep-2,  0x1.736360b19933dp-2,
+    0x1.736360b19933dp-2,  0x1.413c50a25560ep-2,  0x1.c76fb531d2b94p-3,  0x1.9ea1d04ca03aep-4};
+
 struct GL3 {
   static constexpr int n = 3;
   CPB_HD static double x(int i) {
+#ifdef __CUDA_ARCH__
+    return c_gl3[i];
+#else
     return i == 0 ? -0x1.8c97ef43f7248p-1 : (i == 1 ? 0.0 : 0x1.8c97ef43f7248p-1);
+#endif
   }
-  CPB_HD static double w(int i) { return i == 1 ? 0x1.c71c71c71c71cp-1 : 0x1.1c71c71c71c73p-1; }
+  CPB_HD static double w(int i) {
+#ifdef __CUDA_ARCH__
+    return c_gl3[3 + i];
+#else
+    return i == 1 ? 0x1.c71c71c71c71cp-1 : 0x1.1c71c71c71c73p-1;
+#endif
+  }
 };
 
 // Symmetric Gauss-Legendre rules by node count, as (positive node, weight)
@@ -95,6 +116,9 @@ struct GLSym<8> {
 struct GL8 {
   static constexpr int n = 8;
   CPB_HD static double x(int i) {
+#ifdef __CUDA_ARCH__
+    return c_gl8[i];
+#else
     switch (i) {
       case 0: return -0x1.ebab1cb0acc66p-1;
       case 1: return -0x1.97e4ab249f41ep-1;
@@ -105,16 +129,22 @@ struct GL8 {
       case 6: return 0x1.97e4ab249f41ep-1;
       default: return 0x1.ebab1cb0acc66p-1;
     }
+#endif
   }
   CPB_HD static double w(int i) {
+#ifdef __CUDA_ARCH__
+    return c_gl8[8 + i];
+#else
     switch (i) {
       case 0: case 7: return 0x1.9ea1d04ca03aep-4;
       case 1: case 6: return 0x1.c76fb531d2b94p-3;
       case 2: case 5: return 0x1.413c50a25560ep-2;
       default: return 0x1.736360b19933dp-2;
     }
+#endif
   }
 };
+
 
 // ---------------------------------------------------------------------------
 // keyed splitmix64 stream (rngstream.py:18-48)
