@@ -896,11 +896,12 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
 #pragma unroll
     for (int j = 0; j < GL8::n / 2; ++j) {
       const double tau = half * GL8::x(7 - j);
+      const double wpj = GL8::w(j) * pdf0;
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
         const double t = side ? tau : -tau;
         const double uc = fma(t, ih[C_], uc0);
-        const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+        const double wp = wpj * fma(-uc, uc, 1.0);
         double F[5], g[4];
 #pragma unroll
         for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
