@@ -337,10 +337,10 @@ __global__ void __launch_bounds__(2 * kTmaTile) fit_tma_hist2_kernel(
   }
   float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
   bool bad = false;
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % stages;
-    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+  int s = 0;           // ring slot of this tile
+  uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
     const float* col = buf + (size_t)s * rows * kTmaTile + px;
     const int64_t p = t * kTmaTile + px;
     const bool live = p < a.npix;
@@ -403,6 +403,10 @@ __global__ void __launch_bounds__(2 * kTmaTile) fit_tma_hist2_kernel(
       const int64_t tn = t + (int64_t)stages * gridDim.x;
       if (tn < ntiles) issue(tn, s);
     }
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1u;
+    }
   }
   merge_range(vmin, vmax, bad, a.range);
 }
@@ -440,10 +444,10 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
   }
   float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
   bool bad = false;
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % stages;
-    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+  int s = 0;           // ring slot of this tile
+  uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
     const float* col = buf + (size_t)s * rows * kTmaTile + tid;
     const int64_t p = t * kTmaTile + tid;
     if (p < a.npix) {
@@ -531,6 +535,10 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
       const int64_t tn = t + (int64_t)stages * gridDim.x;
       if (tn < ntiles) issue(tn, s);
     }
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1u;
+    }
   }
   merge_range(vmin, vmax, bad, a.range);
 }
@@ -602,10 +610,10 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
   const bool moments = a.mean[0] || a.mean[1];
   float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
   bool bad = false;
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % stages;
-    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+  int s = 0;           // ring slot of this tile
+  uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
     const float* col = buf + (size_t)s * rows * kTmaTile + tid;
     const int64_t p = t * kTmaTile + tid;
     if (p < a.npix) {
@@ -710,6 +718,10 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
       const int64_t tn = t + (int64_t)stages * gridDim.x;
       if (tn < ntiles) issue(tn, s);
     }
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1u;
+    }
   }
   merge_range(vmin, vmax, bad, a.range);
 }
@@ -755,10 +767,10 @@ __global__ void __launch_bounds__(2 * kTmaTile) fit_tma_multi2_kernel(
   }
   float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
   bool bad = false;
-  int k = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    const int s = k % stages;
-    mbar_wait(&full[s], (uint32_t)((k / stages) & 1));
+  int s = 0;           // ring slot of this tile
+  uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&full[s], phase);
     const float* col = buf + (size_t)s * rows * kTmaTile + px;
     const int64_t p = t * kTmaTile + px;
     if (p < a.npix) {
@@ -838,6 +850,10 @@ __global__ void __launch_bounds__(2 * kTmaTile) fit_tma_multi2_kernel(
     if (tid == 0) {
       const int64_t tn = t + (int64_t)stages * gridDim.x;
       if (tn < ntiles) issue(tn, s);
+    }
+    if (++s == stages) {
+      s = 0;
+      phase ^= 1u;
     }
   }
   if (!moment_role) merge_range(vmin, vmax, bad, a.range);
