@@ -251,7 +251,8 @@ CPB_D float fkey_inv(uint32_t u) {
 // pixel's min / max, where raw is 0 and >= h - 1 >= k), then bisection on
 // the keys pins it -- exact for any data, e.g. bins whose edge sits within
 // 1e-17 of zero, where the step is ~2^40 float ulps away from the guess.
-CPB_D float bin_threshold(int k, double lo, double scale, float guess, float vlo, float vhi) {
+CPB_D __noinline__ float bin_threshold_search(int k, double lo, double scale, float guess, float vlo,
+                                              float vhi) {
   const double kk = (double)k;
   auto pred = [&](uint32_t u) {
     return floor(__dmul_rn(__dsub_rn((double)fkey_inv(u), lo), scale)) >= kk;
@@ -286,6 +287,24 @@ CPB_D float bin_threshold(int k, double lo, double scale, float guess, float vlo
     if (pred(mid)) hi_k = mid; else lo_k = mid;
   }
   return fkey_inv(hi_k);
+}
+
+// Fast path: the predicate at the clamped guess and at its neighbour towards
+// the step, straight-line; they differ whenever the guess is within an ulp of
+// the threshold (the usual case), otherwise the out-of-line search above.
+CPB_D float bin_threshold(int k, double lo, double scale, float guess, float vlo, float vhi) {
+  const double kk = (double)k;
+  auto pred = [&](uint32_t u) {
+    return floor(__dmul_rn(__dsub_rn((double)fkey_inv(u), lo), scale)) >= kk;
+  };
+  const uint32_t kmin = fkey(vlo), kmax = fkey(vhi);
+  uint32_t g = fkey(guess);
+  g = g < kmin ? kmin : (g > kmax ? kmax : g);
+  // pred(kmin) is false and pred(kmax) true, so g - 1 / g + 1 stay in range
+  const bool pg = pred(g);
+  const uint32_t n = pg ? g - 1u : g + 1u;
+  if (pg != pred(n)) return fkey_inv(pg ? g : n);
+  return bin_threshold_search(k, lo, scale, guess, vlo, vhi);
 }
 
 CPB_D float bin_threshold(int k, double lo, double scale, float vlo, float vhi) {
