@@ -1913,19 +1913,25 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     const double scale = pdf * half;
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = fma(s[q], scale, acc[q]);
-    // advance every list whose next edge is xn
-    tcp += nextc == xn ? K4 : 0;
-    pdf = tcp[1];
-    nextc = tcp[2 * P + 1];
+    // advance every list whose next edge is xn; only those lanes re-read
+    // their state (predicated loads: shared-memory wavefronts, not the FP64
+    // pipe, were the busiest unit with all five lists re-read every piece)
+    if (nextc == xn) {
+      tcp += K4;
+      pdf = tcp[1];
+      nextc = tcp[2 * P + 1];
+    }
 #pragma unroll
     for (int p = 1; p < 5; ++p) {
-      tp[p] += nx[p] == xn ? K4 : 0;
-      const double2 a = *reinterpret_cast<const double2*>(tp[p]);
-      const double2 b = *reinterpret_cast<const double2*>(tp[p] + 2 * P);
-      cc_[p] = a.x;
-      ss[p] = a.y;
-      ee[p] = b.x;
-      nx[p] = b.y;
+      if (nx[p] == xn) {
+        tp[p] += K4;
+        const double2 a = *reinterpret_cast<const double2*>(tp[p]);
+        const double2 b = *reinterpret_cast<const double2*>(tp[p] + 2 * P);
+        cc_[p] = a.x;
+        ss[p] = a.y;
+        ee[p] = b.x;
+        nx[p] = b.y;
+      }
     }
     x = xn;  // every next edge lies beyond x, so the partition only moves forward
   }
