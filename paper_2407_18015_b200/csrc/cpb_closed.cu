@@ -1747,8 +1747,9 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   const int h = HB <= 8 ? HB : f.bins;
   // [(h + 2) states][2 pairs][P pixels] of double2: (CUM, SL) then (EV, NX), so
   // a list advance is two 16-byte loads (conflict-free: 8 lanes x 16 B)
+  // The EV slot of the below-support state (never read as EV: its SL is 0)
+  // holds the fast-mode flag, 0 when (|lo| + |hi|) / binw <= kFastRatio.
   double* T = sm;
-  double* RATIO = sm + (size_t)(h + 2) * 4 * P;  // (|lo| + |hi|) / binw, fast-mode test
   const int64_t r0 = row_begin + (int64_t)(blockIdx.x / ctiles) * kTabTH;
   const int64_t c0 = (int64_t)(blockIdx.x % ctiles) * kTabTW;  // staged cols [c0, c0 + SW)
   const int tid = threadIdx.y * kTabTW + threadIdx.x;
@@ -1758,7 +1759,9 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   auto build = [&](int i, double lo, double hi, const double* wv) {
     const double it = 1.0 / (HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
-    T[2 * i] = 0.0; T[2 * i + 1] = 0.0; T[2 * P + 2 * i] = 0.0; T[2 * P + 2 * i + 1] = lo;
+    T[2 * i] = 0.0; T[2 * i + 1] = 0.0;
+    T[2 * P + 2 * i] = (fabs(lo) + fabs(hi)) * ibinw <= kFastRatio ? 0.0 : 1.0;
+    T[2 * P + 2 * i + 1] = lo;
     double cum = 0.0;
 #pragma unroll
     for (int b = 0; b < HB; ++b) {
@@ -1774,7 +1777,6 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     }
     double* t = T + (size_t)(h + 1) * 4 * P + 2 * i;
     t[0] = 1.0; t[1] = 0.0; t[2 * P] = 0.0; t[2 * P + 1] = inf;
-    RATIO[i] = (fabs(lo) + fabs(hi)) * ibinw;
   };
   constexpr int NT = kTabTW * kTabTH, NPT = (P + NT - 1) / NT;
   if (HB <= 8 && f.bounds == CPB_BOUNDS_F32_FITTED && f.wmode == CPB_WEIGHTS_U8) {
@@ -1853,9 +1855,8 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   if (r < row_end && c < f.width - 1) {
   const int ic = (threadIdx.y + 1) * SW + threadIdx.x + 1;
   const int ip[5] = {ic, ic + 1, ic - SW, ic - 1, ic + SW};  // C E N W S
-  const bool fast = RATIO[ip[0]] <= kFastRatio && RATIO[ip[1]] <= kFastRatio &&
-                    RATIO[ip[2]] <= kFastRatio && RATIO[ip[3]] <= kFastRatio &&
-                    RATIO[ip[4]] <= kFastRatio;
+  const bool fast = T[2 * P + 2 * ip[0]] + T[2 * P + 2 * ip[1]] + T[2 * P + 2 * ip[2]] +
+                    T[2 * P + 2 * ip[3]] + T[2 * P + 2 * ip[4]] == 0.0;
   constexpr int K4 = 4 * P;
   const double x0 = T[2 * P + 2 * ip[0] + 1];                     // lo_C (NX of state 0)
   const double xend = T[(size_t)h * K4 + 2 * P + 2 * ip[0] + 1];  // hi_C (NX of state h)
@@ -2040,7 +2041,7 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       break;
     }
     case CPB_HISTOGRAM: {
-      const size_t tab_smem = ((size_t)4 * (f.bins + 2) + 1) * kTabP * 8;
+      const size_t tab_smem = (size_t)4 * (f.bins + 2) * kTabP * 8;
       static const int variant = [] { const char* e = getenv("CPB_HIST_VARIANT"); return e ? atoi(e) : 0; }();
       if (variant == 0 && f.bins <= kTabMaxBins && tab_smem <= 200 * 1024) {
         const int ctiles = (int)((f.width - 2 + kTabTW - 1) / kTabTW);
