@@ -947,6 +947,20 @@ struct PPWarpSmem {
   unsigned char fast[32];
 };
 
+// closed_pp_kernel's per-warp layout: ROWS rows of vertex constants (uniform
+// lo, hi, inv; Epanechnikov m, ih, plus the MX float copies), the piece ends,
+// and per slot the (owner lane, neighbour states) word in the r2 slot.  Slot e
+// is read and written only by lane e % 32, so its results overwrite its own
+// (a, b, owner) words, and the vertex's fast-mode flag is the sign of its
+// centre ih (inv) row.  Epanechnikov fp64: 9.25 KB per warp, six 4-warp blocks
+// per SM (24 warps; 12 with PPWarpSmem).
+template <int ROWS>
+struct PPSmem {
+  double vd[ROWS][32];
+  double pa[9 * 32], pb[9 * 32];  // piece ends, then results min / max
+  double r2[9 * 32];              // owner | state << 8, then result saddle (t1 + t2)
+};
+
 struct PPAdaSmem : PPWarpSmem {
   unsigned short slot[9 * 32];  // result slot of a (class-sorted) piece
 };
@@ -1218,7 +1232,9 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     double* psad, double* partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  PPWarpSmem& S = reinterpret_cast<PPWarpSmem*>(smem_raw)[warp];
+  constexpr int ROWS = (KIND == CPB_UNIFORM || MX) ? 15 : 10;
+  constexpr int FR = KIND == CPB_UNIFORM ? 10 : 5;  // centre inv / ih row: sign = !fast
+  PPSmem<ROWS>& S = reinterpret_cast<PPSmem<ROWS>*>(smem_raw)[warp];
   const int64_t v = ((int64_t)blockIdx.x * kPPWarps + warp) * 32 + lane;
   const bool live = v < nvert;
   int64_t idx = 0;
@@ -1226,6 +1242,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   double pts[10];
   int tg[8];
   double mref = 0.0;  // MX: the centre mean, origin of the float coordinates
+  bool vfast = false;
   if (live) {
     const int64_t r = row_begin + v / cols, c = 1 + v % cols;
     idx = r * f.width + c;
@@ -1268,7 +1285,8 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
         }
       }
     }
-    S.fast[lane] = fast ? 1 : 0;
+    if (!fast) S.vd[FR][lane] = -S.vd[FR][lane];
+    vfast = fast;
     double k[8];
 #pragma unroll
     for (int p = 1; p < 5; ++p) {
@@ -1300,15 +1318,14 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
       if (pts[i + 1] > pts[i]) {
-        if (MX && S.fast[lane]) {  // float position in the first word of the slot
+        if (MX && vfast) {  // float position in the first word of the slot
           reinterpret_cast<float*>(&S.pa[q])[0] = (float)(pts[i] - mref);
           reinterpret_cast<float*>(&S.pb[q])[0] = (float)(pts[i + 1] - mref);
         } else {
           S.pa[q] = pts[i];
           S.pb[q] = pts[i + 1];
         }
-        S.owner[q] = (unsigned char)lane;
-        S.state[q] = (unsigned char)cnt;
+        reinterpret_cast<unsigned*>(&S.r2[q])[0] = (unsigned)lane | (cnt << 8);
         ++q;
       }
       if (i < 8) cnt += 1u << (2 * (tg[i] >> 1));
@@ -1316,7 +1333,9 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   }
   __syncwarp();
   for (int e = lane; e < total; e += 32) {
-    const int o = S.owner[e];
+    const unsigned os = reinterpret_cast<const unsigned*>(&S.r2[e])[0];
+    const int o = (int)(os & 0xffu);
+    const bool vf_ = S.vd[FR][o] > 0.0;
     const double a = S.pa[e], b = S.pb[e];
     double s[4];
     bool mk[4];
@@ -1328,11 +1347,11 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
         hi[p] = S.vd[5 + p][o];
         inv[p] = S.vd[10 + p][o];
       }
-      if (S.fast[o]) uniform_piece<true>(a, b, lo, hi, inv, s, mk);
+      if (vf_) uniform_piece<true>(a, b, lo, hi, inv, s, mk);
       else uniform_piece<false>(a, b, lo, hi, inv, s, mk);
     } else {
-      const unsigned st = S.state[e];
-      if (MX && S.fast[o]) {
+      const unsigned st = os >> 8;
+      if (MX && vf_) {
         const float* vf = reinterpret_cast<const float*>(&S.vd[10][0]);
         float mf[5], ihf[5], sf[4];
 #pragma unroll
@@ -1344,36 +1363,37 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
         const float fb = reinterpret_cast<const float*>(&S.pb[e])[0];
         epan_piece_f(fa, fb, mf, ihf, st, sf);
         const double hf = 0.5 * (double)(fb - fa);
-        S.res[e][0] = (double)sf[0] * hf;
-        S.res[e][1] = (double)sf[1] * hf;
-        S.res[e][2] = (double)(sf[2] + sf[3]) * hf;
+        S.pa[e] = (double)sf[0] * hf;
+        S.pb[e] = (double)sf[1] * hf;
+        S.r2[e] = (double)(sf[2] + sf[3]) * hf;
         continue;
       }
       double m[5], ih[5];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
         m[p] = S.vd[p][o];
-        ih[p] = S.vd[5 + p][o];
+        ih[p] = p == 0 ? fabs(S.vd[5][o]) : S.vd[5 + p][o];
       }
-      if (S.fast[o]) epan_piece_st<true>(a, b, m, ih, st, s);
+      if (vf_) epan_piece_st<true>(a, b, m, ih, st, s);
       else epan_piece_st<false>(a, b, m, ih, st, s);
       mk[0] = mk[1] = mk[2] = mk[3] = true;
     }
     const double half = 0.5 * (b - a);
 #pragma unroll
-    S.res[e][0] = mk[0] ? s[0] * half : 0.0;
-    S.res[e][1] = mk[1] ? s[1] * half : 0.0;
-    S.res[e][2] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
+    S.pa[e] = mk[0] ? s[0] * half : 0.0;
+    S.pb[e] = mk[1] ? s[1] * half : 0.0;
+    S.r2[e] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
   }
   __syncwarp();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (live) {
     for (int q = off; q < off + n; ++q) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) acc[r] += S.res[q][r];
+      acc[0] += S.pa[q];
+      acc[1] += S.pb[q];
+      acc[2] += S.r2[q];
     }
     if (KIND == CPB_UNIFORM) {
-      const double pdf = S.vd[10][lane];  // 1 / (hi_C - lo_C)
+      const double pdf = fabs(S.vd[10][lane]);  // 1 / (hi_C - lo_C)
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[r] *= pdf;
     }
@@ -1986,7 +2006,6 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
   static const int pp = [] { const char* e = getenv("CPB_PP"); return e ? atoi(e) : 1; }();
   const int64_t cols = f.width - 2, nvert = rows * cols;
   const int64_t pp_blocks = (nvert + kPPWarps * 32 - 1) / (kPPWarps * 32);
-  const size_t pp_smem = sizeof(PPWarpSmem) * kPPWarps;
   // per-block partial sums of the expected counts (freed on every path)
   struct Partial {
     double* p = nullptr;
@@ -2014,9 +2033,12 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
         break;
       }
       if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
-      cudaFuncSetAttribute(closed_pp_kernel<CPB_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
-      closed_pp_kernel<CPB_UNIFORM><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
-          f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
+      {
+        const size_t pp_smem = sizeof(PPSmem<15>) * kPPWarps;
+        cudaFuncSetAttribute(closed_pp_kernel<CPB_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
+        closed_pp_kernel<CPB_UNIFORM><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
+            f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
+      }
       fused_counts = true;
       break;
     case CPB_EPANECHNIKOV: {
@@ -2034,6 +2056,8 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       }
       if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
       auto kern = f.mixed ? closed_pp_kernel<CPB_EPANECHNIKOV, true> : closed_pp_kernel<CPB_EPANECHNIKOV, false>;
+      const size_t pp_smem = (f.mixed ? sizeof(PPSmem<15>) : sizeof(PPSmem<10>)) * kPPWarps;
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
       kern<<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
           f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
