@@ -455,9 +455,10 @@ CPB_D void uniform_piece(double a, double b, const double* lo, const double* hi,
   range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
 }
 
-// The four integrals (min, max, saddle t1, t2) of one all-uniform
-// neighbourhood given its five supports [lo_P, hi_P] (P = C, E, N, W, S).
-CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) {
+// The four integrals of one all-uniform neighbourhood from its supports and
+// the merged, tagged partition points k / t.
+CPB_D void uniform_integrals_merged(const double* lo, const double* hi, const double* k,
+                                    const int* t, double acc[4]) {
   double inv[5];
   bool fast = true;
 #pragma unroll
@@ -465,6 +466,17 @@ CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) 
     inv[p] = 1.0 / (hi[p] - lo[p]);
     fast &= (fabs(lo[p]) + fabs(hi[p])) * inv[p] <= kFastRatio;
   }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) acc[r] = 0.0;
+  if (fast) uniform_pieces_tagged<true>(lo, hi, inv, k, t, acc);
+  else uniform_pieces_tagged<false>(lo, hi, inv, k, t, acc);
+#pragma unroll
+  for (int r = 0; r < 4; ++r) acc[r] *= inv[C_];
+}
+
+// The four integrals (min, max, saddle t1, t2) of one all-uniform
+// neighbourhood given its five supports [lo_P, hi_P] (P = C, E, N, W, S).
+CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) {
   double k[8];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
@@ -473,12 +485,35 @@ CPB_D void uniform_integrals(const double* lo, const double* hi, double acc[4]) 
   }
   int t[8] = {0, 1, 2, 3, 4, 5, 6, 7};
   merge_pairs8_tagged(k, t);
+  uniform_integrals_merged(lo, hi, k, t, acc);
+}
+
+CPB_D void tcswapf(float& a, float& b, int& ta, int& tb);
+
+// Fitted float supports (not eps-widened): the clamped partition points are
+// floats themselves, so clamping and the tagged merge run exactly on the FP32
+// / integer pipes (FMNMX, FSETP + SEL) instead of FP64 compares.
+CPB_D void uniform_integrals_f32keys(const float* rl, const float* rh, const double* lo,
+                                     const double* hi, double acc[4]) {
+  float kf[8];
+  int t[8];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) acc[r] = 0.0;
-  if (fast) uniform_pieces_tagged<true>(lo, hi, inv, k, t, acc);
-  else uniform_pieces_tagged<false>(lo, hi, inv, k, t, acc);
+  for (int p = 1; p < 5; ++p) {
+    kf[2 * p - 2] = fminf(fmaxf(rl[p], rl[C_]), rh[C_]);
+    kf[2 * p - 1] = fminf(fmaxf(rh[p], rl[C_]), rh[C_]);
+    t[2 * p - 2] = 2 * p - 2;
+    t[2 * p - 1] = 2 * p - 1;
+  }
+  tcswapf(kf[0], kf[2], t[0], t[2]); tcswapf(kf[1], kf[3], t[1], t[3]); tcswapf(kf[1], kf[2], t[1], t[2]);
+  tcswapf(kf[4], kf[6], t[4], t[6]); tcswapf(kf[5], kf[7], t[5], t[7]); tcswapf(kf[5], kf[6], t[5], t[6]);
+  tcswapf(kf[0], kf[4], t[0], t[4]); tcswapf(kf[1], kf[5], t[1], t[5]); tcswapf(kf[2], kf[6], t[2], t[6]);
+  tcswapf(kf[3], kf[7], t[3], t[7]);
+  tcswapf(kf[2], kf[4], t[2], t[4]); tcswapf(kf[3], kf[5], t[3], t[5]);
+  tcswapf(kf[1], kf[2], t[1], t[2]); tcswapf(kf[3], kf[4], t[3], t[4]); tcswapf(kf[5], kf[6], t[5], t[6]);
+  double k[8];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) acc[r] *= inv[C_];
+  for (int q = 0; q < 8; ++q) k[q] = (double)kf[q];
+  uniform_integrals_merged(lo, hi, k, t, acc);
 }
 
 __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
@@ -515,12 +550,15 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
             hi[p] = __dadd_rn(c, he);
           }
         }
+        uniform_integrals(lo, hi, acc);
+      } else {
+        uniform_integrals_f32keys(rl, rh, lo, hi, acc);
       }
     } else {
 #pragma unroll
       for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+      uniform_integrals(lo, hi, acc);
     }
-    uniform_integrals(lo, hi, acc);
     store(pmin, pmax, psad, idx, acc);
   }
   if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
