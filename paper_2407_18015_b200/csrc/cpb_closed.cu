@@ -1807,6 +1807,10 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   // a list advance is two 16-byte loads (conflict-free: 8 lanes x 16 B)
   // The EV slot of the below-support state (never read as EV: its SL is 0)
   // holds the fast-mode flag, 0 when (|lo| + |hi|) / binw <= kFastRatio.
+  // The first pair holds (B, SL / 2): on a fast-mode pixel B = CUM - SL EV,
+  // so on a piece with midpoint sum s2 = a + b the CDF at the midpoint is one
+  // FMA, B + (SL / 2) s2 (|SL EV| <= kFastRatio there bounds the cancellation
+  // to ~1e-14); on the other pixels B = CUM (exact-mode evaluation).
   double* T = sm;
   const int64_t r0 = row_begin + (int64_t)(blockIdx.x / ctiles) * kTabTH;
   const int64_t c0 = (int64_t)(blockIdx.x % ctiles) * kTabTW;  // staged cols [c0, c0 + SW)
@@ -1817,8 +1821,9 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   auto build = [&](int i, double lo, double hi, const double* wv) {
     const double it = 1.0 / (HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
+    const bool pfast = (fabs(lo) + fabs(hi)) * ibinw <= kFastRatio;
     T[2 * i] = 0.0; T[2 * i + 1] = 0.0;
-    T[2 * P + 2 * i] = (fabs(lo) + fabs(hi)) * ibinw <= kFastRatio ? 0.0 : 1.0;
+    T[2 * P + 2 * i] = pfast ? 0.0 : 1.0;
     T[2 * P + 2 * i + 1] = lo;
     double cum = 0.0;
 #pragma unroll
@@ -1826,9 +1831,10 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
       if (b < h) {
         const double wn = wv[b] * it;
         double* t = T + (size_t)(b + 1) * 4 * P + 2 * i;
-        t[0] = cum;
-        t[1] = wn * ibinw;
-        t[2 * P] = fma(binw, (double)b, lo);
+        const double sl = wn * ibinw, ev = fma(binw, (double)b, lo);
+        t[0] = pfast ? fma(-sl, ev, cum) : cum;
+        t[1] = 0.5 * sl;
+        t[2 * P] = ev;
         t[2 * P + 1] = b + 1 < h ? fma(width, (double)(b + 1) / dh, lo) : hi;
         cum += wn;
       }
@@ -1915,6 +1921,9 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   const int ip[5] = {ic, ic + 1, ic - SW, ic - 1, ic + SW};  // C E N W S
   const bool fast = T[2 * P + 2 * ip[0]] + T[2 * P + 2 * ip[1]] + T[2 * P + 2 * ip[2]] +
                     T[2 * P + 2 * ip[3]] + T[2 * P + 2 * ip[4]] == 0.0;
+  bool pf[5];  // per-pixel fast flags (the exact mode reads B = CUM - SL EV there)
+#pragma unroll
+  for (int p = 0; p < 5; ++p) pf[p] = T[2 * P + 2 * ip[p]] == 0.0;
   constexpr int K4 = 4 * P;
   const double x0 = T[2 * P + 2 * ip[0] + 1];                     // lo_C (NX of state 0)
   const double xend = T[(size_t)h * K4 + 2 * P + 2 * ip[0] + 1];  // hi_C (NX of state h)
@@ -1940,18 +1949,20 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   while (x < xend) {
     const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
     // the piece [x, xn]; coincident edges give a zero-width piece worth exactly 0
-    const double half = 0.5 * (xn - x), mid = 0.5 * (xn + x);
+    // (ss = SL / 2, pdf = SL_C / 2: the halves of half and mid are folded in)
+    const double s2 = xn + x, hd = xn - x;
     double s[4];
     if (fast) {
       double Fm[5], d[5];
-      const double tau = half * GL3::x(2);
+      const double tau = hd * GL3::x(2);
 #pragma unroll
       for (int p = 1; p < 5; ++p) {
-        Fm[p] = fma(mid - ee[p], ss[p], cc_[p]);
+        Fm[p] = fma(ss[p], s2, cc_[p]);
         d[p] = tau * ss[p];
       }
       gl3_sym_sums(Fm, d, s);
     } else {
+      const double half = 0.5 * hd, mid = 0.5 * s2;
 #pragma unroll
       for (int q = 0; q < 4; ++q) s[q] = 0.0;
 #pragma unroll
@@ -1959,7 +1970,8 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
         const double xx = node_x(mid, half, GL3::x(j));
         double F[5], g[4];
 #pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = fma(xx - ee[p], ss[p], cc_[p]);
+        for (int p = 1; p < 5; ++p)
+          F[p] = pf[p] ? fma(2.0 * ss[p], xx, cc_[p]) : fma(xx - ee[p], 2.0 * ss[p], cc_[p]);
         integrands(F, g);
 #pragma unroll
         for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(j), g[q], s[q]);
@@ -1969,7 +1981,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     // (a neighbour below its support has F = 0, above it S = 1 - 1 = 0), so
     // the piece adds exactly 0 -- the range limits of engine.py:603-628 are
     // implied by the clipped CDFs.
-    const double scale = pdf * half;
+    const double scale = pdf * hd;
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = fma(s[q], scale, acc[q]);
     // advance every list whose next edge is xn; only those lanes re-read
