@@ -109,6 +109,32 @@ CPB_D void gl3_sym_sums(const double* Fm, const double* d, double s[4]) {
   s[3] = term(snss, fefw);
 }
 
+// gl3_sym_sums with the saddle integrals summed inside: s[2] = t1 + t2 (the
+// stencils only ever report the saddle sum), 37 FP64 operations.
+CPB_D void gl3_sym_sums3(const double* Fm, const double* d, double s[3]) {
+  struct Pair { double p0, pe, po; };
+  auto pair = [](double x0, double dx, double y0, double dy) {
+    Pair r;
+    r.p0 = x0 * y0;
+    r.pe = fma(dx, dy, r.p0);
+    r.po = fma(x0, dy, y0 * dx);
+    return r;
+  };
+  const double sE = 1.0 - Fm[E_], sN = 1.0 - Fm[N_], sW = 1.0 - Fm[W_], sS = 1.0 - Fm[S_];
+  const Pair sesw = pair(sE, -d[E_], sW, -d[W_]), snss = pair(sN, -d[N_], sS, -d[S_]);
+  const Pair fefw = pair(Fm[E_], d[E_], Fm[W_], d[W_]), fnfs = pair(Fm[N_], d[N_], Fm[S_], d[S_]);
+  const double w1 = GL3::w(1), w0x2 = 2.0 * GL3::w(0);
+  auto term = [&](const Pair& P, const Pair& Q) {
+    const double gs = fma(P.po, Q.po, P.pe * Q.pe);
+    return fma(w0x2, gs, w1 * (P.p0 * Q.p0));
+  };
+  s[0] = term(sesw, snss);
+  s[1] = term(fefw, fnfs);
+  const double gs = fma(sesw.po, fnfs.po, fma(sesw.pe, fnfs.pe, fma(snss.po, fefw.po, snss.pe * fefw.pe)));
+  const double g0 = fma(sesw.p0, fnfs.p0, snss.p0 * fefw.p0);
+  s[2] = fma(w0x2, gs, w1 * g0);
+}
+
 // gl3_sym_sums in single precision (the mixed-precision closed form: the
 // partition, node offsets and accumulation stay float64, the per-piece GL3
 // evaluation runs on the FP32 pipes).
@@ -1960,7 +1986,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
         Fm[p] = fma(ss[p], s2, cc_[p]);
         d[p] = tau * ss[p];
       }
-      gl3_sym_sums(Fm, d, s);
+      gl3_sym_sums3(Fm, d, s);
     } else {
       const double half = 0.5 * hd, mid = 0.5 * s2;
 #pragma unroll
@@ -1976,6 +2002,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
 #pragma unroll
         for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(j), g[q], s[q]);
       }
+      s[2] += s[3];
     }
     // No range masks: outside an integral's range some factor is an exact 0
     // (a neighbour below its support has F = 0, above it S = 1 - 1 = 0), so
@@ -1983,7 +2010,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     // implied by the clipped CDFs.
     const double scale = pdf * hd;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = fma(s[q], scale, acc[q]);
+    for (int q = 0; q < 3; ++q) acc[q] = fma(s[q], scale, acc[q]);  // acc[3] stays 0
     // advance every list whose next edge is xn; only those lanes re-read
     // their state (predicated loads: shared-memory wavefronts, not the FP64
     // pipe, were the busiest unit with all five lists re-read every piece)
