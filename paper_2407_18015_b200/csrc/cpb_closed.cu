@@ -78,6 +78,16 @@ CPB_D void integrands(const double* F, double g[4]) {
   g[3] = snss * fefw;
 }
 
+// integrands with the two saddle terms summed: g[2] = t1 + t2
+CPB_D void integrands3(const double* F, double g[3]) {
+  const double sE = 1.0 - F[E_], sN = 1.0 - F[N_], sW = 1.0 - F[W_], sS = 1.0 - F[S_];
+  const double sesw = sE * sW, snss = sN * sS;
+  const double fefw = F[E_] * F[W_], fnfs = F[N_] * F[S_];
+  g[0] = sesw * snss;
+  g[1] = fefw * fnfs;
+  g[2] = fma(sesw, fnfs, snss * fefw);
+}
+
 // GL3 sums of the four integrands on one piece from the neighbour CDFs at
 // the piece midpoint (Fm) and their slopes times the node offset (d): with
 // F = Fm +- d at the nodes mid +- tau, each pair product X*Y is Pe +- Po
@@ -954,7 +964,7 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
     al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (c == 2u ? 1.0 : -1.0);
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) s[r] = 0.0;
+  for (int r = 0; r < 4; ++r) s[r] = 0.0;  // s[2] = t1 + t2, s[3] stays 0
   if (FAST) {
     const double uc0 = (mid - m[C_]) * ih[C_];
 #pragma unroll
@@ -966,12 +976,12 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
         const double t = side ? tau : -tau;
         const double uc = fma(t, ih[C_], uc0);
         const double wp = wpj * fma(-uc, uc, 1.0);
-        double F[5], g[4];
+        double F[5], g[3];
 #pragma unroll
         for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
-        integrands(F, g);
+        integrands3(F, g);
 #pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+        for (int r = 0; r < 3; ++r) s[r] = fma(wp, g[r], s[r]);
       }
     }
   } else {
@@ -980,12 +990,12 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
       const double x = node_x(mid, half, GL8::x(j));
       const double uc = (x - m[C_]) * ih[C_];
       const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-      double F[5], g[4];
+      double F[5], g[3];
 #pragma unroll
       for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
-      integrands(F, g);
+      integrands3(F, g);
 #pragma unroll
-      for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
+      for (int r = 0; r < 3; ++r) s[r] = fma(wp, g[r], s[r]);
     }
   }
 }
