@@ -422,7 +422,8 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
         double d[5];
 #pragma unroll
         for (int p = 1; p < 5; ++p) d[p] = tau * be[p];
-        gl3_sym_sums(al, d, s);
+        gl3_sym_sums3(al, d, s);
+        s[3] = 0.0;
       } else {
         double F[5], g[4];
 #pragma unroll
@@ -436,9 +437,10 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
 #pragma unroll
           for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
         }
+        s[2] += s[3];
       }
 #pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] = fma(s[r], half, acc[r]);
+      for (int r = 0; r < 3; ++r) acc[r] = fma(s[r], half, acc[r]);  // acc[3] stays 0
       a = b;
     }
     if (i < 8) cnt += 1u << (2 * (t[i] >> 1));
