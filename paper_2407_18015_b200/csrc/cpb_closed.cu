@@ -145,6 +145,28 @@ CPB_D void gl3_sym_sums3(const double* Fm, const double* d, double s[3]) {
   s[2] = fma(w0x2, gs, w1 * g0);
 }
 
+// gl3_sym_sums3 before the Gauss-Legendre weights: s = w0x2 gs + w1 g0, the
+// caller accumulates gs and g0 separately and weights the totals once.
+CPB_D void gl3_sym_parts3(const double* Fm, const double* d, double gs[3], double g0[3]) {
+  struct Pair { double p0, pe, po; };
+  auto pair = [](double x0, double dx, double y0, double dy) {
+    Pair r;
+    r.p0 = x0 * y0;
+    r.pe = fma(dx, dy, r.p0);
+    r.po = fma(x0, dy, y0 * dx);
+    return r;
+  };
+  const double sE = 1.0 - Fm[E_], sN = 1.0 - Fm[N_], sW = 1.0 - Fm[W_], sS = 1.0 - Fm[S_];
+  const Pair sesw = pair(sE, -d[E_], sW, -d[W_]), snss = pair(sN, -d[N_], sS, -d[S_]);
+  const Pair fefw = pair(Fm[E_], d[E_], Fm[W_], d[W_]), fnfs = pair(Fm[N_], d[N_], Fm[S_], d[S_]);
+  gs[0] = fma(sesw.po, snss.po, sesw.pe * snss.pe);
+  g0[0] = sesw.p0 * snss.p0;
+  gs[1] = fma(fefw.po, fnfs.po, fefw.pe * fnfs.pe);
+  g0[1] = fefw.p0 * fnfs.p0;
+  gs[2] = fma(sesw.po, fnfs.po, fma(sesw.pe, fnfs.pe, fma(snss.po, fefw.po, snss.pe * fefw.pe)));
+  g0[2] = fma(sesw.p0, fnfs.p0, snss.p0 * fefw.p0);
+}
+
 // gl3_sym_sums in single precision (the mixed-precision closed form: the
 // partition, node offsets and accumulation stay float64, the per-piece GL3
 // evaluation runs on the FP32 pipes).
@@ -1954,6 +1976,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   __syncthreads();
   const int64_t r = r0 + threadIdx.y, c = c0 + 1 + threadIdx.x;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  double accs[3] = {0.0, 0.0, 0.0};  // fast mode: node-pair sums (acc holds the midpoint ones)
   if (r < row_end && c < f.width - 1) {
   const int ic = (threadIdx.y + 1) * SW + threadIdx.x + 1;
   const int ip[5] = {ic, ic + 1, ic - SW, ic - 1, ic + SW};  // C E N W S
@@ -1990,6 +2013,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     // (ss = SL / 2, pdf = SL_C / 2: the halves of half and mid are folded in)
     const double s2 = xn + x, hd = xn - x;
     double s[4];
+    const double scale = pdf * hd;
     if (fast) {
       double Fm[5], d[5];
       const double tau = hd * GL3::x(2);
@@ -1998,7 +2022,10 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
         Fm[p] = fma(ss[p], s2, cc_[p]);
         d[p] = tau * ss[p];
       }
-      gl3_sym_sums3(Fm, d, s);
+      double gs[3];
+      gl3_sym_parts3(Fm, d, gs, s);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) accs[q] = fma(gs[q], scale, accs[q]);
     } else {
       const double half = 0.5 * hd, mid = 0.5 * s2;
 #pragma unroll
@@ -2020,7 +2047,6 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     // (a neighbour below its support has F = 0, above it S = 1 - 1 = 0), so
     // the piece adds exactly 0 -- the range limits of engine.py:603-628 are
     // implied by the clipped CDFs.
-    const double scale = pdf * hd;
 #pragma unroll
     for (int q = 0; q < 3; ++q) acc[q] = fma(s[q], scale, acc[q]);  // acc[3] stays 0
     // advance every list whose next edge is xn; only those lanes re-read
@@ -2044,6 +2070,11 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
       }
     }
     x = xn;  // every next edge lies beyond x, so the partition only moves forward
+  }
+  if (fast) {  // the Gauss-Legendre weights, once per vertex
+    const double w1 = GL3::w(1), w0x2 = 2.0 * GL3::w(0);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) acc[q] = fma(w0x2, accs[q], w1 * acc[q]);
   }
   store(pmin, pmax, psad, r * f.width + c, acc);
   }
