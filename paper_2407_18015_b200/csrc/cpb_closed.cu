@@ -425,6 +425,7 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
                                  const double* k, const int* t, double acc[4]) {
   double a = lo[C_];
   unsigned cnt = 0;  // 2 bits per neighbour p at bit 2 (p - 1)
+  double accs[3] = {0.0, 0.0, 0.0};  // FAST: node-pair sums (acc: midpoint sums)
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
     const double b = i < 8 ? k[i] : hi[C_];
@@ -444,8 +445,10 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
         double d[5];
 #pragma unroll
         for (int p = 1; p < 5; ++p) d[p] = tau * be[p];
-        gl3_sym_sums3(al, d, s);
-        s[3] = 0.0;
+        double gs[3];
+        gl3_sym_parts3(al, d, gs, s);
+#pragma unroll
+        for (int r = 0; r < 3; ++r) accs[r] = fma(gs[r], half, accs[r]);
       } else {
         double F[5], g[4];
 #pragma unroll
@@ -466,6 +469,11 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
       a = b;
     }
     if (i < 8) cnt += 1u << (2 * (t[i] >> 1));
+  }
+  if (FAST) {  // the Gauss-Legendre weights, once per vertex
+    const double w1 = GL3::w(1), w0x2 = 2.0 * GL3::w(0);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) acc[r] = fma(w0x2, accs[r], w1 * acc[r]);
   }
 }
 
