@@ -2015,7 +2015,10 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   const double* tcp = T + K4 + 2 * ip[0];
   double pdf = tcp[1], nextc = tcp[2 * P + 1];
   double x = x0;
-  while (x < xend) {
+  // x reaches xend exactly when the centre list leaves its last bin (its
+  // next edge bounds every xn), so the loop test is a pointer compare
+  const double* const tend = T + (size_t)(h + 1) * K4 + 2 * ip[0];
+  while (tcp != tend) {
     const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
     // the piece [x, xn]; coincident edges give a zero-width piece worth exactly 0
     // (ss = SL / 2, pdf = SL_C / 2: the halves of half and mid are folded in)
