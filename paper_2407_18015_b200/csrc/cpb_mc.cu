@@ -36,6 +36,13 @@ struct McArgs {
 template <int KIND, int RNG>
 __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a) {
   extern __shared__ double s_tab[];  // per warp: 5 x (h wn + h+1 cum)
+  // two-stage sampling for the costly inverse CDFs (see below): a 64-entry
+  // ring per warp of candidate draws (C value, sample index, type, u_N)
+  constexpr bool kSplit = KIND == CPB_EPANECHNIKOV || KIND == CPB_HISTOGRAM;
+  constexpr int kQ = kSplit ? kMcWarps * 64 : 1;
+  __shared__ double q_x[kQ], q_u[kQ];
+  __shared__ int64_t q_i[kQ];
+  __shared__ unsigned char q_t[kQ];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int h = f.bins;
   const int tab = 2 * h + 1;
@@ -94,7 +101,88 @@ __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a
       for (int q = 0; q < 5 * per; ++q) key[q] = plane_key(pk, (uint64_t)q);
     }
     uint32_t cmin = 0, cmax = 0, csad = 0;
-    for (int64_t i = lane; i < a.n; i += 32) {
+    if (kSplit) {
+      // Two stages: every pattern needs C against E and W on the same side
+      // (min: both less, max: both greater, saddle: either), so a joint
+      // draw first samples C, E, W; only the candidates (~half on most
+      // vertices) are queued, warp-compacted, and draw N and S 32 at a time.
+      // Same samples, same strict comparisons: the counts are unchanged.
+      double* qx = q_x + warp * 64;
+      double* qu = q_u + warp * 64;
+      int64_t* qi = q_i + warp * 64;
+      unsigned char* qt = q_t + warp * 64;
+      int qh = 0, qn = 0;  // warp-uniform ring head and length
+      const uint2 k2 = make_uint2((uint32_t)a.seed, (uint32_t)(a.seed >> 32));
+      auto philox_u = [&](int64_t i, int q, double& lo_u, double& hi_u) {
+        const uint4 o = philox4x32_10(
+            make_uint4((uint32_t)i, (uint32_t)((uint64_t)i >> 32) ^ ((uint32_t)q << 24),
+                       (uint32_t)px, (uint32_t)(px >> 32)), k2);
+        lo_u = u53_from(o.x, o.y);
+        hi_u = u53_from(o.z, o.w);
+      };
+      auto stage2 = [&](int cnt) {
+        if (lane < cnt) {
+          const int e = (qh + lane) & 63;
+          const int64_t i = qi[e];
+          const double x0 = qx[e];
+          double u2, u4, unused;
+          if (RNG == CPB_RNG_SPLITMIX) {
+            u2 = stream_u01(key[2], (uint64_t)i);
+            u4 = stream_u01(key[4], (uint64_t)i);
+          } else {
+            u2 = qu[e];
+            philox_u(i, 2, u4, unused);
+          }
+          const double x2 = draw<KIND>(s[2], u2, 0.0, h), x4 = draw<KIND>(s[4], u4, 0.0, h);
+          const bool lns = x0 < x2 && x0 < x4, gns = x0 > x2 && x0 > x4;
+          if (qt[e] == 1) {
+            cmin += lns;
+            csad += gns;
+          } else {
+            cmax += gns;
+            csad += lns;
+          }
+        }
+        qh = (qh + cnt) & 63;
+        qn -= cnt;
+      };
+      for (int64_t base = 0; base < a.n; base += 32) {
+        const int64_t i = base + lane;
+        int ty = 0;
+        double x0 = 0.0, u2 = 0.0;
+        if (i < a.n) {
+          double u0, u1, u3;
+          if (RNG == CPB_RNG_SPLITMIX) {
+            u0 = stream_u01(key[0], (uint64_t)i);
+            u1 = stream_u01(key[1], (uint64_t)i);
+            u3 = stream_u01(key[3], (uint64_t)i);
+          } else {
+            philox_u(i, 0, u0, u1);
+            philox_u(i, 1, u2, u3);
+          }
+          x0 = draw<KIND>(s[0], u0, 0.0, h);
+          const double x1 = draw<KIND>(s[1], u1, 0.0, h), x3 = draw<KIND>(s[3], u3, 0.0, h);
+          ty = (x0 < x1 && x0 < x3) ? 1 : ((x0 > x1 && x0 > x3) ? 2 : 0);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ty != 0);
+        if (ty) {
+          const int e = (qh + qn + __popc(m & ((1u << lane) - 1u))) & 63;
+          qx[e] = x0;
+          qi[e] = i;
+          qt[e] = (unsigned char)ty;
+          if (RNG != CPB_RNG_SPLITMIX) qu[e] = u2;
+        }
+        qn += __popc(m);
+        __syncwarp();
+        if (qn >= 32) {
+          stage2(32);
+          __syncwarp();
+        }
+      }
+      if (qn > 0) stage2(qn);
+      __syncwarp();
+    }
+    for (int64_t i = kSplit ? a.n : lane; i < a.n; i += 32) {
       double u[10];
       if (RNG == CPB_RNG_SPLITMIX) {
 #pragma unroll
