@@ -73,13 +73,17 @@ CPB_D double hist_cdf_at(const double* wn, const double* cum, double lo, double 
 // the CDF is continuous, so a bin index off by one where (x - lo) / binw
 // rounds across an integer changes the value only by rounding, and the
 // quotient itself by an ulp).
+// The position in bin units t = (x - lo) / binw is clamped to [0, h] first, so
+// the bin is its integer part (capped at h - 1) and the in-bin fraction t - j
+// stays in [0, 1]: the value is then in [0, cum[h - 1] + wn[h - 1]] and only
+// the top needs the clip (binw is unused: kept for the signature).
 CPB_D double hist_cdf_fast(const double* wn, const double* cum, double lo, double binw,
                            double ibinw, int h, double x) {
-  const double t = floor((x - lo) * ibinw);
-  const int j = (int)fmax(0.0, fmin(t, (double)(h - 1)));
-  const double frac = (x - fma(binw, (double)j, lo)) * ibinw;
-  const double v = fma(wn[j], frac, cum[j]);
-  return fmin(fmax(v, 0.0), 1.0);
+  (void)binw;
+  const double t = fmin(fmax((x - lo) * ibinw, 0.0), (double)h);
+  const int j = min((int)t, h - 1);
+  const double v = fma(wn[j], t - (double)j, cum[j]);
+  return fmin(v, 1.0);
 }
 
 }  // namespace cpb
