@@ -266,6 +266,26 @@ def test_monte_carlo_counts_against_oracle(kind, bins):
             assert diff.max() <= 1 and diff.sum() <= 3, (kind, ch, diff.max(), diff.sum())
 
 
+@pytest.mark.parametrize("n", [1, 5, 31, 32, 33, 64, 95])
+def test_monte_carlo_two_stage_small_n(n):
+    """Histogram MC (two-stage draws, warp-compacted candidates) at sample
+    counts around the warp width, and on a constant field (ties everywhere):
+    counts bit-identical to the oracle's."""
+    vals = orc.ackley_ensemble(19, 13, 20, noise_amp=0.3, seed=5)
+    flat = np.repeat(vals[:, :1, :1], 13, axis=1).repeat(19, axis=2)
+    for v in (vals, flat):
+        ref_counts = {}
+        orc.classify(orc.fit(v, "histogram", 4), "histogram", method="monte_carlo", n_samples=n,
+                     seed=31, counts_out=ref_counts)
+        holder = {}
+        cpb.classify_field(_fit(v, "histogram", 4),
+                           cpb.EstimatorSpec(method="monte_carlo", n_samples=n, seed=31),
+                           counts_out=holder)
+        got = holder["counts"].cpu().numpy()
+        for i, ch in enumerate(("min", "max", "saddle")):
+            assert np.array_equal(got[i], ref_counts[ch]), (n, ch)
+
+
 def test_monte_carlo_vs_closed_form_binomial_bound():
     # test_acceptance.py:75-97 style: |p_mc - p_closed| <= 4 SE for >= 99% of vertices
     vals = orc.ackley_ensemble(64, 64, 20, noise_amp=0.3, seed=0)
