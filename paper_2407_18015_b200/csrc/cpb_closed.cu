@@ -1862,6 +1862,118 @@ CPB_D double pairwise16(const double* w, int n) {
   return res;
 }
 
+// The merged sweep of one vertex over its five state-table lists (see
+// closed_hist_tab_kernel).  FAST (all five pixels fast-mode): midpoint CDFs
+// B + (SL/2) s2 and symmetric node pairs; the lists then never need EV, so an
+// advance reads (B, SL/2) and NX only.
+template <bool FAST>
+CPB_D void hist_sweep(const double* T, int h, const int* ip, const bool* pf, double acc[4]) {
+  constexpr int P = kTabP;
+  double accs[3] = {0.0, 0.0, 0.0};  // FAST: node-pair sums (acc holds the midpoint ones)
+  constexpr int K4 = 4 * P;
+  const double x0 = T[2 * P + 2 * ip[0] + 1];                     // lo_C (NX of state 0)
+  // each list is a pointer to its current state's table column; advancing
+  // is one predicated add of the state stride
+  const double* tp[5];
+  double cc_[5], ss[5], ee[5], nx[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    const double* t = T + 2 * ip[p];
+    while (t[2 * P + 1] <= x0) t += K4;
+    tp[p] = t;
+    const double2 a = *reinterpret_cast<const double2*>(t);
+    cc_[p] = a.x;
+    ss[p] = a.y;
+    if (FAST) {
+      ee[p] = 0.0;
+      nx[p] = t[2 * P + 1];
+    } else {
+      const double2 b = *reinterpret_cast<const double2*>(t + 2 * P);
+      ee[p] = b.x;
+      nx[p] = b.y;
+    }
+  }
+  const double* tcp = T + K4 + 2 * ip[0];
+  double pdf = tcp[1], nextc = tcp[2 * P + 1];
+  double x = x0;
+  // x reaches hi_C exactly when the centre list leaves its last bin (its
+  // next edge bounds every xn), so the loop test is a pointer compare
+  const double* const tend = T + (size_t)(h + 1) * K4 + 2 * ip[0];
+  while (tcp != tend) {
+    const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
+    // the piece [x, xn]; coincident edges give a zero-width piece worth exactly 0
+    // (ss = SL / 2, pdf = SL_C / 2: the halves of half and mid are folded in)
+    const double s2 = xn + x, hd = xn - x;
+    double s[4];
+    const double scale = pdf * hd;
+    if (FAST) {
+      double Fm[5], d[5];
+      const double tau = hd * GL3::x(2);
+#pragma unroll
+      for (int p = 1; p < 5; ++p) {
+        Fm[p] = fma(ss[p], s2, cc_[p]);
+        d[p] = tau * ss[p];
+      }
+      double gs[3];
+      gl3_sym_parts3(Fm, d, gs, s);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) accs[q] = fma(gs[q], scale, accs[q]);
+    } else {
+      const double half = 0.5 * hd, mid = 0.5 * s2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s[q] = 0.0;
+#pragma unroll
+      for (int j = 0; j < GL3::n; ++j) {
+        const double xx = node_x(mid, half, GL3::x(j));
+        double F[5], g[4];
+#pragma unroll
+        for (int p = 1; p < 5; ++p)
+          F[p] = pf[p] ? fma(2.0 * ss[p], xx, cc_[p]) : fma(xx - ee[p], 2.0 * ss[p], cc_[p]);
+        integrands(F, g);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(j), g[q], s[q]);
+      }
+      s[2] += s[3];
+    }
+    // No range masks: outside an integral's range some factor is an exact 0
+    // (a neighbour below its support has F = 0, above it S = 1 - 1 = 0), so
+    // the piece adds exactly 0 -- the range limits of engine.py:603-628 are
+    // implied by the clipped CDFs.
+#pragma unroll
+    for (int q = 0; q < 3; ++q) acc[q] = fma(s[q], scale, acc[q]);  // acc[3] stays 0
+    // advance every list whose next edge is xn; only those lanes re-read
+    // their state (predicated loads: shared-memory wavefronts, not the FP64
+    // pipe, were the busiest unit with all five lists re-read every piece)
+    if (nextc == xn) {
+      tcp += K4;
+      pdf = tcp[1];
+      nextc = tcp[2 * P + 1];
+    }
+#pragma unroll
+    for (int p = 1; p < 5; ++p) {
+      if (nx[p] == xn) {
+        tp[p] += K4;
+        const double2 a = *reinterpret_cast<const double2*>(tp[p]);
+        cc_[p] = a.x;
+        ss[p] = a.y;
+        if (FAST) {
+          nx[p] = tp[p][2 * P + 1];
+        } else {
+          const double2 b = *reinterpret_cast<const double2*>(tp[p] + 2 * P);
+          ee[p] = b.x;
+          nx[p] = b.y;
+        }
+      }
+    }
+    x = xn;  // every next edge lies beyond x, so the partition only moves forward
+  }
+  if (FAST) {  // the Gauss-Legendre weights, once per vertex
+    const double w1 = GL3::w(1), w0x2 = 2.0 * GL3::w(0);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) acc[q] = fma(w0x2, accs[q], w1 * acc[q]);
+  }
+}
+
 // HB: bin count when <= 8 (compile-time: exact-size staging loops), else 16
 // (runtime bins 9..16).
 template <int HB>
@@ -1984,7 +2096,6 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   __syncthreads();
   const int64_t r = r0 + threadIdx.y, c = c0 + 1 + threadIdx.x;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  double accs[3] = {0.0, 0.0, 0.0};  // fast mode: node-pair sums (acc holds the midpoint ones)
   if (r < row_end && c < f.width - 1) {
   const int ic = (threadIdx.y + 1) * SW + threadIdx.x + 1;
   const int ip[5] = {ic, ic + 1, ic - SW, ic - 1, ic + SW};  // C E N W S
@@ -1993,100 +2104,8 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   bool pf[5];  // per-pixel fast flags (the exact mode reads B = CUM - SL EV there)
 #pragma unroll
   for (int p = 0; p < 5; ++p) pf[p] = T[2 * P + 2 * ip[p]] == 0.0;
-  constexpr int K4 = 4 * P;
-  const double x0 = T[2 * P + 2 * ip[0] + 1];                     // lo_C (NX of state 0)
-  const double xend = T[(size_t)h * K4 + 2 * P + 2 * ip[0] + 1];  // hi_C (NX of state h)
-  // each list is a pointer to its current state's table column; advancing
-  // is one predicated add of the state stride
-  const double* tp[5];
-  double cc_[5], ss[5], ee[5], nx[5];
-#pragma unroll
-  for (int p = 1; p < 5; ++p) {
-    const double* t = T + 2 * ip[p];
-    while (t[2 * P + 1] <= x0) t += K4;
-    tp[p] = t;
-    const double2 a = *reinterpret_cast<const double2*>(t);
-    const double2 b = *reinterpret_cast<const double2*>(t + 2 * P);
-    cc_[p] = a.x;
-    ss[p] = a.y;
-    ee[p] = b.x;
-    nx[p] = b.y;
-  }
-  const double* tcp = T + K4 + 2 * ip[0];
-  double pdf = tcp[1], nextc = tcp[2 * P + 1];
-  double x = x0;
-  // x reaches xend exactly when the centre list leaves its last bin (its
-  // next edge bounds every xn), so the loop test is a pointer compare
-  const double* const tend = T + (size_t)(h + 1) * K4 + 2 * ip[0];
-  while (tcp != tend) {
-    const double xn = dmin(dmin(nextc, dmin(nx[E_], nx[N_])), dmin(nx[W_], nx[S_]));
-    // the piece [x, xn]; coincident edges give a zero-width piece worth exactly 0
-    // (ss = SL / 2, pdf = SL_C / 2: the halves of half and mid are folded in)
-    const double s2 = xn + x, hd = xn - x;
-    double s[4];
-    const double scale = pdf * hd;
-    if (fast) {
-      double Fm[5], d[5];
-      const double tau = hd * GL3::x(2);
-#pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        Fm[p] = fma(ss[p], s2, cc_[p]);
-        d[p] = tau * ss[p];
-      }
-      double gs[3];
-      gl3_sym_parts3(Fm, d, gs, s);
-#pragma unroll
-      for (int q = 0; q < 3; ++q) accs[q] = fma(gs[q], scale, accs[q]);
-    } else {
-      const double half = 0.5 * hd, mid = 0.5 * s2;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) s[q] = 0.0;
-#pragma unroll
-      for (int j = 0; j < GL3::n; ++j) {
-        const double xx = node_x(mid, half, GL3::x(j));
-        double F[5], g[4];
-#pragma unroll
-        for (int p = 1; p < 5; ++p)
-          F[p] = pf[p] ? fma(2.0 * ss[p], xx, cc_[p]) : fma(xx - ee[p], 2.0 * ss[p], cc_[p]);
-        integrands(F, g);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) s[q] = fma(GL3::w(j), g[q], s[q]);
-      }
-      s[2] += s[3];
-    }
-    // No range masks: outside an integral's range some factor is an exact 0
-    // (a neighbour below its support has F = 0, above it S = 1 - 1 = 0), so
-    // the piece adds exactly 0 -- the range limits of engine.py:603-628 are
-    // implied by the clipped CDFs.
-#pragma unroll
-    for (int q = 0; q < 3; ++q) acc[q] = fma(s[q], scale, acc[q]);  // acc[3] stays 0
-    // advance every list whose next edge is xn; only those lanes re-read
-    // their state (predicated loads: shared-memory wavefronts, not the FP64
-    // pipe, were the busiest unit with all five lists re-read every piece)
-    if (nextc == xn) {
-      tcp += K4;
-      pdf = tcp[1];
-      nextc = tcp[2 * P + 1];
-    }
-#pragma unroll
-    for (int p = 1; p < 5; ++p) {
-      if (nx[p] == xn) {
-        tp[p] += K4;
-        const double2 a = *reinterpret_cast<const double2*>(tp[p]);
-        const double2 b = *reinterpret_cast<const double2*>(tp[p] + 2 * P);
-        cc_[p] = a.x;
-        ss[p] = a.y;
-        ee[p] = b.x;
-        nx[p] = b.y;
-      }
-    }
-    x = xn;  // every next edge lies beyond x, so the partition only moves forward
-  }
-  if (fast) {  // the Gauss-Legendre weights, once per vertex
-    const double w1 = GL3::w(1), w0x2 = 2.0 * GL3::w(0);
-#pragma unroll
-    for (int q = 0; q < 3; ++q) acc[q] = fma(w0x2, accs[q], w1 * acc[q]);
-  }
+  if (fast) hist_sweep<true>(T, h, ip, pf, acc);
+  else hist_sweep<false>(T, h, ip, pf, acc);
   store(pmin, pmax, psad, r * f.width + c, acc);
   }
   if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
