@@ -1998,9 +1998,19 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   const double inf = __longlong_as_double(0x7ff0000000000000ll);
   const double dh = (double)h, invM = 1.0 / (double)f.members;
   // per-pixel state tables from (lo, hi, raw weights)
+  // (short dependency chains: this build runs once per staged pixel and its
+  // latency, with the barrier after it, is exposed at the start of a tile)
+  const double ih = 1.0 / dh;
+  auto rcp = [](double v) {  // 1 / v to ~1 ulp: FP32 estimate + two Newton steps
+    const float e = __frcp_rn((float)v);
+    if (!(fabsf(e) > 1e-37f && fabsf(e) < 1e37f)) return 1.0 / v;  // outside FP32 range
+    double r = (double)e;
+    r = r * fma(-v, r, 2.0);
+    return r * fma(-v, r, 2.0);
+  };
   auto build = [&](int i, double lo, double hi, const double* wv) {
-    const double it = 1.0 / (HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
-    const double width = hi - lo, binw = width / dh, ibinw = 1.0 / binw;
+    const double it = rcp(HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
+    const double width = hi - lo, binw = width * ih, ibinw = dh * rcp(width);
     const bool pfast = (fabs(lo) + fabs(hi)) * ibinw <= kFastRatio;
     T[2 * i] = 0.0; T[2 * i + 1] = 0.0;
     T[2 * P + 2 * i] = pfast ? 0.0 : 1.0;
