@@ -1878,8 +1878,14 @@ CPB_D void hist_sweep(const double* T, int h, const int* ip, const bool* pf, dou
   double cc_[5], ss[5], ee[5], nx[5];
 #pragma unroll
   for (int p = 1; p < 5; ++p) {
+    // first state whose next edge lies beyond lo_C: the first three edges
+    // tested with independent loads (one shared-memory latency for all four
+    // lists), the rare rest by walking
     const double* t = T + 2 * ip[p];
-    while (t[2 * P + 1] <= x0) t += K4;
+    const int k = (t[2 * P + 1] <= x0) + (t[K4 + 2 * P + 1] <= x0) + (t[2 * K4 + 2 * P + 1] <= x0);
+    t += k * K4;
+    if (k == 3)
+      while (t[2 * P + 1] <= x0) t += K4;
     tp[p] = t;
     const double2 a = *reinterpret_cast<const double2*>(t);
     cc_[p] = a.x;
