@@ -100,7 +100,10 @@ def peaks():
 # clocks
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi polling during the timed region: SM clock (median of the busy
+    samples), max SM clock and the throttle reasons seen."""
+
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -108,27 +111,53 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.path = f"/tmp/cpb_clocks_{os.getpid()}.csv"
+        self.window = None
 
     def start(self):
+        """Start polling every 100 ms and wait for the first sample, so that even a
+        short timed region right after this call is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        deadline = time.time() + 10.0
+        while time.time() < deadline and self.proc.poll() is None and os.path.getsize(self.path) == 0:
+            time.sleep(0.05)
+
+    def mark(self, begin, end):
+        """Wall-clock window of the timed region; samples outside it are dropped."""
+        self.window = (begin, end)
 
     def stop(self):
+        import datetime
+
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)  # one more polling period past the window's end
         self.proc.terminate()
         self.proc.wait(timeout=10)
-        sm, smax, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        rows = []
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
             if len(f) < 9:
                 continue
+            try:
+                t = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                t = None
+            rows.append((t, f))
+        keep = rows
+        if self.window and rows:
+            b, e = self.window
+            inside = [r for r in rows if r[0] is not None and b - 0.1 <= r[0] <= e + 0.1]
+            keep = inside or rows
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for _, f in keep:
             try:
                 sm.append(float(f[1]))
                 smax = float(f[2])
@@ -295,11 +324,13 @@ def run_ours(args):
     clocks.start()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
     t0.record()
     for _ in range(args.steps):
         step()
     t1.record()
     torch.cuda.synchronize()
+    clocks.mark(wall0, time.time())
     barrier()
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
