@@ -2014,8 +2014,11 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
     r = r * fma(-v, r, 2.0);
     return r * fma(-v, r, 2.0);
   };
-  auto build = [&](int i, double lo, double hi, const double* wv) {
-    const double it = rcp(HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
+  // unit_sum: the weights are member counts / M (or one-hot), whose sum is 1 to
+  // a few ulps, so the renormalisation w / sum(w) (engine.py:538-540) is the
+  // identity to within the closed form's tolerance and is skipped
+  auto build = [&](int i, double lo, double hi, const double* wv, bool unit_sum) {
+    const double it = unit_sum ? 1.0 : rcp(HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width * ih, ibinw = dh * rcp(width);
     const bool pfast = (fabs(lo) + fabs(hi)) * ibinw <= kFastRatio;
     T[2 * i] = 0.0; T[2 * i + 1] = 0.0;
@@ -2078,7 +2081,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
         const unsigned cnt = rc[j][q < HC ? q : 0];
         wv[q] = q < h ? (deg ? (q == dbin ? 1.0 : 0.0) : (double)cnt * invM) : 0.0;
       }
-      build(tid + j * NT, lo, hi, wv);
+      build(tid + j * NT, lo, hi, wv, true);
     }
   } else {
     for (int i = tid; i < P; i += NT) {
@@ -2106,7 +2109,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
         }
         wv[b] = wb;
       }
-      build(i, lo, hi, wv);
+      build(i, lo, hi, wv, false);
     }
   }
   __syncthreads();
