@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
         if (NT > 0) {
           // cumulative counts C_k = #{v >= thr_k}; bin b holds C_b - C_{b+1}
           float thr[NB];
-          const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)h);
+          const float step = __fsub_rn(hi, lo) * __frcp_rn((float)h);  // a guess: any rounding
 #pragma unroll
           for (int q = 1; q < NB; ++q)
             thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
       if (hist) {
         const double dlo = (double)lo;
         const double scale = __ddiv_rn((double)a.bins, __dsub_rn((double)hi, dlo));
-        const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)a.bins);
+        const float step = __fsub_rn(hi, lo) * __frcp_rn((float)a.bins);  // a guess: any rounding
 #pragma unroll
         for (int q = 1; q < NB; ++q) {
           thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(2 * kTmaTile) fit_tma_multi2_kernel(
           constexpr int NB = NT > 0 ? NT : 1;
           const double dlo = (double)lo;
           const double scale = __ddiv_rn((double)a.bins, __dsub_rn((double)hi, dlo));
-          const float step = __fdiv_rn(__fsub_rn(hi, lo), (float)a.bins);
+          const float step = __fsub_rn(hi, lo) * __frcp_rn((float)a.bins);  // a guess: any rounding
           uint32_t c[NB + 1];
           float thr[NB];
 #pragma unroll
