@@ -466,6 +466,15 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
   }
   if (e != cudaSuccess) return cuda_status(e, "stream setup");
   cudaStream_t s0 = ss.s[0], scls = sx.s[0], scopy = sx.s[1];
+  size_t max_pitch = 0;
+  {
+    int dev = 0, mp = 0;
+    e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mp, cudaDevAttrMaxPitch, dev);
+    if (e != cudaSuccess) return cuda_status(e, "device attribute");
+    max_pitch = (size_t)(unsigned)mp;
+    if (const char* v = getenv("CPB_HOST_MAX_PITCH")) max_pitch = (size_t)atoll(v);  // tests
+  }
   const size_t plane = (size_t)height * width;
   const size_t row_bytes = (size_t)members * width * sizeof(float);
   static const size_t chunk_bytes = [] {  // CPB_HOST_CHUNK_BYTES overrides, for tests
@@ -543,11 +552,13 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     if (method == 0) return cpb_classify_closed(&f, r0, r1, om, oM, oS, st);
     return cpb_classify_mc(&f, r0, r1, seed, n_samples, CPB_RNG_SPLITMIX, om, oM, oS, nullptr, st);
   };
+  // unrequested channels are never computed: their host planes are zeroed on
+  // the host instead (the reference leaves them exactly 0.0, test_engine.py:616-623)
   auto copy_rows = [&](int i, int64_t r0, int64_t r1) -> int {
     const double* base = (const double*)out[i].p;
     for (int c = 0; c < 3; ++c) {
       double* dst = h_out ? h_out[3 * i + c] : nullptr;
-      if (!dst || r1 <= r0) continue;
+      if (!dst || r1 <= r0 || !(channels & (1u << c))) continue;
       const size_t off = (size_t)r0 * width, n = (size_t)(r1 - r0) * width;
       cudaError_t ce = cudaMemcpyAsync(dst + off, base + c * plane + off, n * sizeof(double),
                                        cudaMemcpyDeviceToHost, scopy);
@@ -572,10 +583,18 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
     const int64_t r0 = j * chunk, nr = std::min(chunk, height - r0);
     const int b = (int)(j & 1);
     cudaStream_t st = ss.s[b];
-    // one 2-D copy: M member rows of nr*W floats, source pitch = member plane
-    e = cudaMemcpy2DAsync(ebuf[b].p, (size_t)nr * width * sizeof(float), h_ens + r0 * width,
-                          plane * sizeof(float), (size_t)nr * width * sizeof(float), (size_t)members,
-                          cudaMemcpyHostToDevice, st);
+    // one 2-D copy: M member rows of nr*W floats, source pitch = member plane;
+    // a member plane wider than the driver's maximum pitch (grids of >= 2^29
+    // pixels) goes as one plain copy per member instead
+    if (plane * sizeof(float) <= max_pitch) {
+      e = cudaMemcpy2DAsync(ebuf[b].p, (size_t)nr * width * sizeof(float), h_ens + r0 * width,
+                            plane * sizeof(float), (size_t)nr * width * sizeof(float), (size_t)members,
+                            cudaMemcpyHostToDevice, st);
+    } else {
+      for (int64_t m = 0; m < members && e == cudaSuccess; ++m)
+        e = cudaMemcpyAsync((float*)ebuf[b].p + m * nr * width, h_ens + m * plane + r0 * width,
+                            (size_t)nr * width * sizeof(float), cudaMemcpyHostToDevice, st);
+    }
     if (e != cudaSuccess) return cuda_status(e, "H2D ensemble chunk");
     tmark(st);
     if (j > 0) {  // range accumulation is serialised across the ring by chunk order
@@ -638,6 +657,10 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
   for (int i = 0; i < nm; ++i)
     for (int c = 0; c < 3; ++c)
       if (double* dst = h_out ? h_out[3 * i + c] : nullptr) {
+        if (!(channels & (1u << c))) {
+          memset(dst, 0, plane * sizeof(double));
+          continue;
+        }
         memset(dst, 0, (size_t)width * sizeof(double));
         memset(dst + (size_t)(height - 1) * width, 0, (size_t)width * sizeof(double));
       }

@@ -37,15 +37,6 @@ CPB_D void cswap(double& a, double& b) {
   b = hi;
 }
 
-// Batcher merge of four sorted (lo, hi) pairs: 15 compare-exchanges.
-CPB_D void merge_pairs8(double* k) {
-  cswap(k[0], k[2]); cswap(k[1], k[3]); cswap(k[1], k[2]);
-  cswap(k[4], k[6]); cswap(k[5], k[7]); cswap(k[5], k[6]);
-  cswap(k[0], k[4]); cswap(k[1], k[5]); cswap(k[2], k[6]); cswap(k[3], k[7]);
-  cswap(k[2], k[4]); cswap(k[3], k[5]);
-  cswap(k[1], k[2]); cswap(k[3], k[4]); cswap(k[5], k[6]);
-}
-
 // Ranges of the four integrals (engine.py:603-628):
 //   min : [lo_C, min(all hi)]                         factors S_E S_N S_W S_S
 //   max : [max(all lo), hi_C]                         factors F_E F_N F_W F_S
@@ -347,55 +338,6 @@ CPB_D double piece_end(const double* k, double hiC, int i) {
 }
 
 // ----------------------------------------------------------------- uniform
-// pdf_C = 1/(hi_C - lo_C); F_P(x) = clip((x - lo_P)/(hi_P - lo_P), 0, 1)
-// (engine.py:510-520), 3-node Gauss-Legendre per piece (integrand degree 4).
-template <bool FAST>
-CPB_D void uniform_pieces(const double* lo, const double* hi, const double* inv, const double* k,
-                          double acc[4]) {
-  double a = lo[C_];
-#pragma unroll 1
-  for (int i = 0; i < 9; ++i) {
-    const double b = piece_end(k, hi[C_], i);
-    if (b > a) {
-      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-      bool bl[5], ab[5];
-      double al[5], be[5];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
-        const bool in = !(bl[p] | ab[p]);
-        be[p] = in ? inv[p] : 0.0;
-        al[p] = in ? (FAST ? (mid - lo[p]) * inv[p] : 0.0) : (ab[p] ? 1.0 : 0.0);
-      }
-      double s[4], F[5], g[4];
-      if (FAST) {
-        const double tau = half * GL3::x(2);
-        double d[5];
-#pragma unroll
-        for (int p = 1; p < 5; ++p) d[p] = tau * be[p];
-        gl3_sym_sums(al, d, s);
-      } else {
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = 0.0;
-#pragma unroll
-        for (int j = 0; j < GL3::n; ++j) {
-          const double x = node_x(mid, half, GL3::x(j));
-#pragma unroll
-          for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
-          integrands(F, g);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
-        }
-      }
-      bool m[4];
-      range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], m);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] = m[r] ? fma(s[r], half, acc[r]) : acc[r];
-    }
-    a = dmax(a, b);
-  }
-}
-
 // Batcher merge of four sorted (key, tag) pairs: one compare per exchange,
 // the tag (2 (p - 1) + {0: lo, 1: hi}) travels with its key.
 CPB_D void tcswap(double& a, double& b, int& ta, int& tb) {
@@ -475,52 +417,6 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
 #pragma unroll
     for (int r = 0; r < 3; ++r) acc[r] = fma(w0x2, accs[r], w1 * acc[r]);
   }
-}
-
-// One uniform piece [a, b]: s[r] = GL3 sum of integrand r (before half, pdf).
-template <bool FAST>
-CPB_D void uniform_piece(double a, double b, const double* lo, const double* hi, const double* inv,
-                         double s[4], bool mk[4]) {
-  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-  bool bl[5], ab[5];
-  double al[5], be[5];
-#pragma unroll
-  for (int p = 1; p < 5; ++p) {
-    piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
-    const bool in = !(bl[p] | ab[p]);
-    be[p] = in ? inv[p] : 0.0;
-    al[p] = in ? (FAST ? (mid - lo[p]) * inv[p] : 0.0) : (ab[p] ? 1.0 : 0.0);
-  }
-  double F[5], g[4];
-  if (FAST) {
-    const double tau = half * GL3::x(2);
-#pragma unroll
-    for (int p = 1; p < 5; ++p) F[p] = al[p];
-    integrands(F, g);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) s[r] = GL3::w(1) * g[r];
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-#pragma unroll
-      for (int p = 1; p < 5; ++p) F[p] = fma(side ? tau : -tau, be[p], al[p]);
-      integrands(F, g);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(0), g[r], s[r]);
-    }
-  } else {
-#pragma unroll
-    for (int r = 0; r < 4; ++r) s[r] = 0.0;
-#pragma unroll
-    for (int j = 0; j < GL3::n; ++j) {
-      const double x = node_x(mid, half, GL3::x(j));
-#pragma unroll
-      for (int p = 1; p < 5; ++p) F[p] = fma(x - lo[p], be[p], al[p]);
-      integrands(F, g);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) s[r] = fma(GL3::w(j), g[r], s[r]);
-    }
-  }
-  range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
 }
 
 // The four integrals of one all-uniform neighbourhood from its supports and
@@ -837,149 +733,6 @@ __global__ void __launch_bounds__(kCombWarps * 32) combinatorial_kernel(
 // cubic gives exactly 0 or 1.
 CPB_D double epan_cdf(double u) { return fma(u, fma(-0.25, u * u, 0.75), 0.5); }
 
-template <bool FAST>
-CPB_D void epan_pieces(const double* m, const double* ih, const double* lo, const double* hi,
-                       const double* k, double acc[4]) {
-  const double pdf0 = 0.75 * ih[C_];
-  double a = lo[C_];
-#pragma unroll 1
-  for (int i = 0; i < 9; ++i) {
-    const double b = piece_end(k, hi[C_], i);
-    if (b > a) {
-      const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-      bool bl[5], ab[5];
-      double al[5], be[5];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
-        const bool in = !(bl[p] | ab[p]);
-        be[p] = in ? ih[p] : 0.0;
-        al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (ab[p] ? 1.0 : -1.0);
-      }
-      const double uc0 = (mid - m[C_]) * ih[C_];
-      double s[4] = {0.0, 0.0, 0.0, 0.0};
-      if (FAST) {
-#pragma unroll
-        for (int j = 0; j < GL8::n / 2; ++j) {
-          const double tau = half * GL8::x(7 - j);
-#pragma unroll
-          for (int side = 0; side < 2; ++side) {
-            const double t = side ? tau : -tau;
-            const double uc = fma(t, ih[C_], uc0);
-            const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-            double F[5], g[4];
-#pragma unroll
-            for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
-            integrands(F, g);
-#pragma unroll
-            for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < GL8::n; ++j) {
-          const double x = node_x(mid, half, GL8::x(j));
-          const double uc = (x - m[C_]) * ih[C_];
-          const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-          double F[5], g[4];
-#pragma unroll
-          for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
-          integrands(F, g);
-#pragma unroll
-          for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-        }
-      }
-      bool mk[4];
-      range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] = mk[r] ? fma(s[r], half, acc[r]) : acc[r];
-    }
-    a = dmax(a, b);
-  }
-}
-
-__global__ void __launch_bounds__(kClosedThreads) closed_epan_kernel(
-    FieldView f, Window w, double* pmin, double* pmax, double* psad) {
-  int64_t idx;
-  if (!vertex(f, w, idx)) return;
-  const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
-  double m[5], ih[5], lo[5], hi[5];
-  bool fast = true;
-#pragma unroll
-  for (int p = 0; p < 5; ++p) {
-    double hw;
-    load_epan(f, at[p], m[p], hw);
-    ih[p] = 1.0 / hw;
-    lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
-    hi[p] = m[p] + hw;
-    fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
-  }
-  double k[8];
-#pragma unroll
-  for (int p = 1; p < 5; ++p) {
-    k[2 * p - 2] = dmin(dmax(lo[p], lo[C_]), hi[C_]);
-    k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
-  }
-  merge_pairs8(k);
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (fast) epan_pieces<true>(m, ih, lo, hi, k, acc);
-  else epan_pieces<false>(m, ih, lo, hi, k, acc);
-  store(pmin, pmax, psad, idx, acc);
-}
-
-// One Epanechnikov piece [a, b]: s[r] = GL8 sum of integrand r (before the
-// factor half), with the piece's range-membership mask.
-template <bool FAST>
-CPB_D void epan_piece(double a, double b, const double* m, const double* ih, const double* lo,
-                      const double* hi, double s[4], bool mk[4]) {
-  const double pdf0 = 0.75 * ih[C_];
-  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-  bool bl[5], ab[5];
-  double al[5], be[5];
-#pragma unroll
-  for (int p = 1; p < 5; ++p) {
-    piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
-    const bool in = !(bl[p] | ab[p]);
-    be[p] = in ? ih[p] : 0.0;
-    al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (ab[p] ? 1.0 : -1.0);
-  }
-#pragma unroll
-  for (int r = 0; r < 4; ++r) s[r] = 0.0;
-  if (FAST) {
-    const double uc0 = (mid - m[C_]) * ih[C_];
-#pragma unroll
-    for (int j = 0; j < GL8::n / 2; ++j) {
-      const double tau = half * GL8::x(7 - j);
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const double t = side ? tau : -tau;
-        const double uc = fma(t, ih[C_], uc0);
-        const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-        double F[5], g[4];
-#pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
-        integrands(F, g);
-#pragma unroll
-        for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < GL8::n; ++j) {
-      const double x = node_x(mid, half, GL8::x(j));
-      const double uc = (x - m[C_]) * ih[C_];
-      const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-      double F[5], g[4];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
-      integrands(F, g);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-    }
-  }
-  range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
-}
-
 // epan_piece with the neighbour states given (2 bits each, from the merge
 // tags: 0 below, 1 inside, 2 above) instead of midpoint comparisons.
 template <bool FAST>
@@ -1042,16 +795,6 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
 // sums its own pieces in piece order, so the result is deterministic and equal
 // to the one-vertex-per-lane kernel's summation order.
 constexpr int kPPWarps = 4;
-constexpr int kPPFields = 18;  // m[5], ih[5], lo[1..4], hi[1..4]
-
-struct PPWarpSmem {
-  double vd[kPPFields][32];  // vertex constants, SoA
-  double pa[9 * 32], pb[9 * 32];
-  double res[9 * 32][3];  // per piece: min, max, saddle (t1 + t2)
-  unsigned char owner[9 * 32];
-  unsigned char state[9 * 32];  // per piece: 2-bit below / inside / above state of E, N, W, S
-  unsigned char fast[32];
-};
 
 // closed_pp_kernel's per-warp layout: ROWS rows of vertex constants (uniform
 // lo, hi, inv; Epanechnikov m, ih, plus the MX float copies), the piece ends,
@@ -1059,228 +802,13 @@ struct PPWarpSmem {
 // is read and written only by lane e % 32, so its results overwrite its own
 // (a, b, owner) words, and the vertex's fast-mode flag is the sign of its
 // centre ih (inv) row.  Epanechnikov fp64: 9.25 KB per warp, six 4-warp blocks
-// per SM (24 warps; 12 with PPWarpSmem).
+// per SM (24 warps).
 template <int ROWS>
 struct PPSmem {
   double vd[ROWS][32];
   double pa[9 * 32], pb[9 * 32];  // piece ends, then results min / max
   double r2[9 * 32];              // owner | state << 8, then result saddle (t1 + t2)
 };
-
-struct PPAdaSmem : PPWarpSmem {
-  unsigned short slot[9 * 32];  // result slot of a (class-sorted) piece
-};
-
-// Degree-adaptive fast-mode Epanechnikov piece: NN symmetric GL nodes (exact
-// for the piece's integrand degree 2 + 3k, see GLSym).
-template <int NN>
-CPB_D void epan_piece_fast_n(double a, double b, const double* m, const double* ih,
-                             const double* lo, const double* hi, double s[4], bool mk[4]) {
-  const double pdf0 = 0.75 * ih[C_];
-  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
-  bool bl[5], ab[5];
-  double al[5], be[5];
-#pragma unroll
-  for (int p = 1; p < 5; ++p) {
-    piece_flags(mid, lo[p], hi[p], bl[p], ab[p]);
-    const bool in = !(bl[p] | ab[p]);
-    be[p] = in ? ih[p] : 0.0;
-    al[p] = in ? (mid - m[p]) * ih[p] : (ab[p] ? 1.0 : -1.0);
-  }
-  const double uc0 = (mid - m[C_]) * ih[C_];
-#pragma unroll
-  for (int r = 0; r < 4; ++r) s[r] = 0.0;
-  if (NN & 1) {  // centre node
-    const double wp = GLSym<NN>::w0() * (pdf0 * fma(-uc0, uc0, 1.0));
-    double F[5], g[4];
-#pragma unroll
-    for (int p = 1; p < 5; ++p) F[p] = epan_cdf(al[p]);
-    integrands(F, g);
-#pragma unroll
-    for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-  }
-#pragma unroll
-  for (int j = 0; j < GLSym<NN>::pairs; ++j) {
-    const double tau = half * GLSym<NN>::x(j);
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const double t = side ? tau : -tau;
-      const double uc = fma(t, ih[C_], uc0);
-      const double wp = GLSym<NN>::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-      double F[5], g[4];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
-      integrands(F, g);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) s[r] = fma(wp, g[r], s[r]);
-    }
-  }
-  range_masks(bl[E_], bl[N_], bl[W_], bl[S_], ab[E_], ab[N_], ab[W_], ab[S_], mk);
-}
-
-// Piece-parallel AND degree-adaptive Epanechnikov stencil.  On a piece where
-// only k of the four neighbour CDFs are non-constant the integrands have
-// degree 2 + 3k, so 2, 3, 5, 6 or 8 Gauss-Legendre nodes are exact (the
-// reference always uses 8, engine.py:600-601; the difference is rounding).
-// The warp sorts its compacted piece list by k (counting sort with warp
-// scans) and evaluates class by class, so every round runs one node count on
-// all 32 lanes.  Pieces of exact-mode vertices keep the 8-node exact path.
-__global__ void __launch_bounds__(kPPWarps * 32) closed_epan_ada_kernel(
-    FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
-    double* psad) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  PPAdaSmem& S = reinterpret_cast<PPAdaSmem*>(smem_raw)[warp];
-  const int64_t v = ((int64_t)blockIdx.x * kPPWarps + warp) * 32 + lane;
-  const bool live = v < nvert;
-  int64_t idx = 0;
-  int n = 0;
-  double pts[10];
-  double lo[5], hi[5];
-  bool fast = true;
-  if (live) {
-    const int64_t r = row_begin + v / cols, c = 1 + v % cols;
-    idx = r * f.width + c;
-    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
-    double m[5], ih[5];
-#pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      double hw;
-      load_epan(f, at[p], m[p], hw);
-      ih[p] = 1.0 / hw;
-      lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
-      hi[p] = m[p] + hw;
-      fast &= (fabs(m[p]) + hw) * ih[p] <= kFastRatio;
-    }
-#pragma unroll
-    for (int p = 0; p < 5; ++p) {
-      S.vd[p][lane] = m[p];
-      S.vd[5 + p][lane] = ih[p];
-    }
-#pragma unroll
-    for (int p = 1; p < 5; ++p) {
-      S.vd[9 + p][lane] = lo[p];
-      S.vd[13 + p][lane] = hi[p];
-    }
-    S.fast[lane] = fast ? 1 : 0;
-    double k[8];
-#pragma unroll
-    for (int p = 1; p < 5; ++p) {
-      k[2 * p - 2] = dmin(dmax(lo[p], lo[C_]), hi[C_]);
-      k[2 * p - 1] = dmin(dmax(hi[p], lo[C_]), hi[C_]);
-    }
-    merge_pairs8(k);
-    pts[0] = lo[C_];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) pts[q + 1] = k[q];
-    pts[9] = hi[C_];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) n += pts[i + 1] > pts[i] ? 1 : 0;
-  }
-  // class of a piece: number of neighbours inside their support (5 = exact mode)
-  auto piece_class = [&](double a, double b) {
-    if (!fast) return 5;
-    const double mid = 0.5 * (b + a);
-    int kk = 0;
-#pragma unroll
-    for (int p = 1; p < 5; ++p) kk += (mid > lo[p] && mid < hi[p]) ? 1 : 0;
-    return kk;
-  };
-  int cnt[6] = {0, 0, 0, 0, 0, 0};
-  if (live) {
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      if (pts[i + 1] > pts[i]) {
-        const int cl = piece_class(pts[i], pts[i + 1]);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) cnt[q] += q == cl ? 1 : 0;
-      }
-    }
-  }
-  // warp scans: slot offsets (original order) and class-sorted positions
-  int off = n;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, off, d);
-    if (lane >= d) off += y;
-  }
-  off -= n;
-  int pos[6], base = 0, ctot[6];
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    int x = cnt[q];
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, x, d);
-      if (lane >= d) x += y;
-    }
-    ctot[q] = __shfl_sync(0xffffffffu, x, 31);
-    pos[q] = base + x - cnt[q];
-    base += ctot[q];
-  }
-  if (live) {
-    int j = 0;
-#pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      if (pts[i + 1] > pts[i]) {
-        const int cl = piece_class(pts[i], pts[i + 1]);
-        int e = 0;
-#pragma unroll
-        for (int q = 0; q < 6; ++q)
-          if (q == cl) e = pos[q]++;
-        S.pa[e] = pts[i];
-        S.pb[e] = pts[i + 1];
-        S.owner[e] = (unsigned char)lane;
-        S.slot[e] = (unsigned short)(off + j);
-        ++j;
-      }
-    }
-  }
-  __syncwarp();
-  int cbase = 0;
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    for (int e = cbase + lane; e < cbase + ctot[q]; e += 32) {
-      const int o = S.owner[e];
-      double m[5], ih[5], plo[5], phi[5];
-#pragma unroll
-      for (int p = 0; p < 5; ++p) {
-        m[p] = S.vd[p][o];
-        ih[p] = S.vd[5 + p][o];
-      }
-#pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        plo[p] = S.vd[9 + p][o];
-        phi[p] = S.vd[13 + p][o];
-      }
-      const double a = S.pa[e], b = S.pb[e];
-      double s[4];
-      bool mk[4];
-      if (q == 0) epan_piece_fast_n<2>(a, b, m, ih, plo, phi, s, mk);
-      else if (q == 1) epan_piece_fast_n<3>(a, b, m, ih, plo, phi, s, mk);
-      else if (q == 2) epan_piece_fast_n<5>(a, b, m, ih, plo, phi, s, mk);
-      else if (q == 3) epan_piece_fast_n<6>(a, b, m, ih, plo, phi, s, mk);
-      else if (q == 4) epan_piece_fast_n<8>(a, b, m, ih, plo, phi, s, mk);
-      else epan_piece<false>(a, b, m, ih, plo, phi, s, mk);
-      const double half = 0.5 * (b - a);
-      const int sl = S.slot[e];
-#pragma unroll
-      S.res[sl][0] = mk[0] ? s[0] * half : 0.0;
-      S.res[sl][1] = mk[1] ? s[1] * half : 0.0;
-      S.res[sl][2] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
-    }
-    cbase += ctot[q];
-  }
-  __syncwarp();
-  if (live) {
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int q = off; q < off + n; ++q) {
-#pragma unroll
-      for (int r = 0; r < 3; ++r) acc[r] += S.res[q][r];
-    }
-    store(pmin, pmax, psad, idx, acc);
-  }
-}
 
 // Mixed-precision Epanechnikov piece (CPB_FLAG_MIXED): positions re-centred on
 // the centre mean in float64 by the owner lane, the 8-node evaluation in FP32.
@@ -1330,16 +858,15 @@ CPB_D void epan_piece_f(float a, float b, const float* m, const float* ih, unsig
   }
 }
 
-// KIND = CPB_UNIFORM (vertex constants lo[5], hi[5], inv[5]) or
-// CPB_EPANECHNIKOV (m[5], ih[5], lo[1..4], hi[1..4]).
-template <int KIND, bool MX = false>
+// Vertex constants m[5], ih[5] (+ MX: their float copies re-centred on m_C).
+template <bool MX>
 __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
     double* psad, double* partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int ROWS = (KIND == CPB_UNIFORM || MX) ? 15 : 10;
-  constexpr int FR = KIND == CPB_UNIFORM ? 10 : 5;  // centre inv / ih row: sign = !fast
+  constexpr int ROWS = MX ? 15 : 10;
+  constexpr int FR = 5;  // centre ih row: sign = !fast
   PPSmem<ROWS>& S = reinterpret_cast<PPSmem<ROWS>*>(smem_raw)[warp];
   const int64_t v = ((int64_t)blockIdx.x * kPPWarps + warp) * 32 + lane;
   const bool live = v < nvert;
@@ -1355,17 +882,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
     double lo[5], hi[5];
     bool fast = true;
-    if (KIND == CPB_UNIFORM) {
-#pragma unroll
-      for (int p = 0; p < 5; ++p) {
-        load_bounds(f, at[p], lo[p], hi[p]);
-        const double inv = 1.0 / (hi[p] - lo[p]);
-        fast &= (fabs(lo[p]) + fabs(hi[p])) * inv <= kFastRatio;
-        S.vd[p][lane] = lo[p];
-        S.vd[5 + p][lane] = hi[p];
-        S.vd[10 + p][lane] = inv;
-      }
-    } else {
+    {
       double m[5], ih[5];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
@@ -1444,18 +961,7 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
     const bool vf_ = S.vd[FR][o] > 0.0;
     const double a = S.pa[e], b = S.pb[e];
     double s[4];
-    bool mk[4];
-    if (KIND == CPB_UNIFORM) {
-      double lo[5], hi[5], inv[5];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) {
-        lo[p] = S.vd[p][o];
-        hi[p] = S.vd[5 + p][o];
-        inv[p] = S.vd[10 + p][o];
-      }
-      if (vf_) uniform_piece<true>(a, b, lo, hi, inv, s, mk);
-      else uniform_piece<false>(a, b, lo, hi, inv, s, mk);
-    } else {
+    {
       const unsigned st = os >> 8;
       if (MX && vf_) {
         const float* vf = reinterpret_cast<const float*>(&S.vd[10][0]);
@@ -1482,13 +988,11 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
       }
       if (vf_) epan_piece_st<true>(a, b, m, ih, st, s);
       else epan_piece_st<false>(a, b, m, ih, st, s);
-      mk[0] = mk[1] = mk[2] = mk[3] = true;
     }
     const double half = 0.5 * (b - a);
-#pragma unroll
-    S.pa[e] = mk[0] ? s[0] * half : 0.0;
-    S.pb[e] = mk[1] ? s[1] * half : 0.0;
-    S.r2[e] = (mk[2] ? s[2] * half : 0.0) + (mk[3] ? s[3] * half : 0.0);
+    S.pa[e] = s[0] * half;
+    S.pb[e] = s[1] * half;
+    S.r2[e] = s[2] * half + s[3] * half;
   }
   __syncwarp();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1497,11 +1001,6 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
       acc[0] += S.pa[q];
       acc[1] += S.pb[q];
       acc[2] += S.r2[q];
-    }
-    if (KIND == CPB_UNIFORM) {
-      const double pdf = fabs(S.vd[10][lane]);  // 1 / (hi_C - lo_C)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) acc[r] *= pdf;
     }
     store(pmin, pmax, psad, idx, acc);
   }
@@ -2171,8 +1670,6 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     set_error("grid too large for one launch (%lld blocks)", (long long)blocks);
     return CPB_EINVAL;
   }
-  // CPB_PP=0 selects the one-vertex-per-lane kernels (A/B experiments)
-  static const int pp = [] { const char* e = getenv("CPB_PP"); return e ? atoi(e) : 1; }();
   const int64_t cols = f.width - 2, nvert = rows * cols;
   const int64_t pp_blocks = (nvert + kPPWarps * 32 - 1) / (kPPWarps * 32);
   // per-block partial sums of the expected counts (freed on every path)
@@ -2190,41 +1687,19 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
   bool fused_counts = false;  // set by the kernels that write block partials
   switch (f.kind) {
     case CPB_UNIFORM:
-      // 3-node pieces are too cheap to amortise the redistribution (measured
-      // 18.6 ms per-lane vs 25.4 ms piece-parallel at 16384^2): per-lane by default
-      if (pp != 2) {
-        if (int rc = want_partial(blocks * (kClosedThreads / 32))) return rc;
-        if (f.mixed)
-          closed_uniform_f32_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
-        else
-          closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
-        fused_counts = true;
-        break;
-      }
-      if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
-      {
-        const size_t pp_smem = sizeof(PPSmem<15>) * kPPWarps;
-        cudaFuncSetAttribute(closed_pp_kernel<CPB_UNIFORM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
-        closed_pp_kernel<CPB_UNIFORM><<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
-            f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
-      }
+      // one vertex per lane: 3-node pieces are too cheap to amortise a
+      // piece-parallel redistribution (measured 18.6 vs 25.4 ms at 16384^2)
+      if (int rc = want_partial(blocks * (kClosedThreads / 32))) return rc;
+      if (f.mixed)
+        closed_uniform_f32_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
+      else
+        closed_uniform_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad, part.p);
       fused_counts = true;
       break;
     case CPB_EPANECHNIKOV: {
-      if (!pp) {
-        closed_epan_kernel<<<(unsigned)blocks, kClosedThreads, 0, st>>>(f, w, pmin, pmax, psad);
-        break;
-      }
-      if (pp == 3) {  // piece-parallel + degree-adaptive node counts (per-warp classes:
-                      // the per-class round padding ate the saving, 59.6 vs 38 ms; kept for A/B)
-        const size_t ada_smem = sizeof(PPAdaSmem) * kPPWarps;
-        cudaFuncSetAttribute(closed_epan_ada_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ada_smem);
-        closed_epan_ada_kernel<<<(unsigned)pp_blocks, kPPWarps * 32, ada_smem, st>>>(
-            f, row_begin, nvert, cols, pmin, pmax, psad);
-        break;
-      }
+      // piece-parallel (8-node pieces): each warp compacts its lanes' non-empty pieces
       if (int rc = want_partial(pp_blocks * kPPWarps)) return rc;
-      auto kern = f.mixed ? closed_pp_kernel<CPB_EPANECHNIKOV, true> : closed_pp_kernel<CPB_EPANECHNIKOV, false>;
+      auto kern = f.mixed ? closed_pp_kernel<true> : closed_pp_kernel<false>;
       const size_t pp_smem = (f.mixed ? sizeof(PPSmem<15>) : sizeof(PPSmem<10>)) * kPPWarps;
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
@@ -2235,8 +1710,7 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     }
     case CPB_HISTOGRAM: {
       const size_t tab_smem = (size_t)4 * (f.bins + 2) * kTabP * 8;
-      static const int variant = [] { const char* e = getenv("CPB_HIST_VARIANT"); return e ? atoi(e) : 0; }();
-      if (variant == 0 && f.bins <= kTabMaxBins && tab_smem <= 200 * 1024) {
+      if (f.bins <= kTabMaxBins && tab_smem <= 200 * 1024) {
         const int ctiles = (int)((f.width - 2 + kTabTW - 1) / kTabTW);
         const int64_t rtiles = (rows + kTabTH - 1) / kTabTH;
         auto kern = closed_hist_tab_kernel<16>;
@@ -2269,9 +1743,7 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       wh.ntiles = (int)((f.width - 2 + tw - 1) / tw);
       const int64_t hb = rows * wh.ntiles;
       const size_t smem = ((size_t)(3 + f.bins) * 3 * (tw + 2) + f.bins + 1) * 8;
-      // CPB_HIST_MINB picks the register budget variant (experiments; default 3 blocks/SM)
-      static const int minb = [] { const char* e = getenv("CPB_HIST_MINB"); return e ? atoi(e) : 4; }();
-      auto kern = minb >= 6 ? closed_hist_smem_kernel<6> : (minb == 5 ? closed_hist_smem_kernel<5> : (minb == 4 ? closed_hist_smem_kernel<4> : closed_hist_smem_kernel<3>));
+      auto kern = closed_hist_smem_kernel<4>;
       if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       kern<<<(unsigned)hb, tw, smem, st>>>(f, wh, pmin, pmax, psad);
@@ -2283,7 +1755,7 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
   }
   CPB_CHECK_LAUNCH("closed-form kernel");
   if (counts) {
-    if (!fused_counts) {  // A/B kernel variants: reduce the written rows instead
+    if (!fused_counts) {  // the large-bin histogram kernels: reduce the written rows instead
       const int64_t nb = std::min<int64_t>(4096, (nvert + 255) / 256);
       if (int rc = want_partial(nb * 8)) return rc;
       rows_partial_kernel<<<(unsigned)nb, 256, 0, st>>>(pmin, pmax, psad, row_begin, cols, f.width,

@@ -314,122 +314,6 @@ CPB_D float bin_threshold(int k, double lo, double scale, float vlo, float vhi) 
 
 // NT: histogram bin count handled with NT-1 register thresholds (1..kThreshBins),
 // or 0 for the shared-memory counters (more bins).
-// Histogram fit with two threads per pixel (the bin counts and min/max are
-// order-free, unlike the Epanechnikov sums): thread halves take members
-// [0, M/2) and [M/2, M) of the staged tile, exchange min/max through shared
-// memory, both derive the same exact thresholds, count their halves and add.
-// Twice the warps per SM of fit_tma_kernel for the compare-heavy binning.
-template <int NT>
-__global__ void __launch_bounds__(2 * kTmaTile) fit_tma_hist2_kernel(
-    const __grid_constant__ CUtensorMap map, FitArgs a, int stages, int mbox, int nbox,
-    int64_t ntiles) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  static_assert(NT >= 1, "threshold path only");
-  const int M = a.members, h = a.bins;
-  const int rows = mbox * nbox;
-  const int tid = threadIdx.x, px = tid % kTmaTile, half = tid / kTmaTile;
-  const int m0 = half ? M / 2 : 0, m1 = half ? M : M / 2;
-  float* buf = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * rows * kTmaTile * 4);
-  float* xlo = reinterpret_cast<float*>(full + stages);  // [2][kTmaTile]
-  float* xhi = xlo + 2 * kTmaTile;
-  uint32_t* xc = reinterpret_cast<uint32_t*>(xhi + 2 * kTmaTile);  // [NT][kTmaTile] from half 1
-  if (tid == 0) {
-    prefetch_tensormap(&map);
-    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const uint64_t pol = policy_evict_first();
-  const uint32_t tile_bytes = (uint32_t)rows * kTmaTile * 4u;
-  auto issue = [&](int64_t tile, int s) {
-    mbar_arrive_expect_tx(&full[s], tile_bytes);
-    float* dst = buf + (size_t)s * rows * kTmaTile;
-    for (int b = 0; b < nbox; ++b)
-      tma_load_2d(dst + (size_t)b * mbox * kTmaTile, &map, (int)(tile * kTmaTile), b * mbox, &full[s], pol);
-  };
-  if (tid == 0) {
-    for (int k = 0; k < stages; ++k) {
-      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
-      if (t < ntiles) issue(t, k);
-    }
-  }
-  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
-  bool bad = false;
-  int s = 0;           // ring slot of this tile
-  uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    mbar_wait(&full[s], phase);
-    const float* col = buf + (size_t)s * rows * kTmaTile + px;
-    const int64_t p = t * kTmaTile + px;
-    const bool live = p < a.npix;
-    float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
-    if (live) {
-#pragma unroll 8
-      for (int m = m0; m < m1; ++m) {
-        const float x = col[m * kTmaTile];
-        bad |= nonfinite(x);
-        lo = fminf(lo, x);
-        hi = fmaxf(hi, x);
-      }
-    }
-    xlo[half * kTmaTile + px] = lo;
-    xhi[half * kTmaTile + px] = hi;
-    __syncthreads();
-    lo = fminf(xlo[px], xlo[kTmaTile + px]);
-    hi = fmaxf(xhi[px], xhi[kTmaTile + px]);
-    vmin = fminf(vmin, lo);
-    vmax = fmaxf(vmax, hi);
-    uint32_t c[NT + 1];
-#pragma unroll
-    for (int q = 0; q <= NT; ++q) c[q] = 0u;
-    const bool flat = !(hi > lo);
-    if (live && !flat) {
-      const double dlo = (double)lo;
-      const double scale = __ddiv_rn((double)h, __dsub_rn((double)hi, dlo));
-      float thr[NT];
-#pragma unroll
-      for (int q = 1; q < NT; ++q) thr[q] = bin_threshold(q, dlo, scale, lo, hi);
-#pragma unroll 4
-      for (int m = m0; m < m1; ++m) {
-        const float x = col[m * kTmaTile];
-#pragma unroll
-        for (int q = 1; q < NT; ++q) c[q] += (x >= thr[q]) ? 1u : 0u;
-      }
-    }
-    if (half) {
-#pragma unroll
-      for (int q = 1; q < NT; ++q) xc[q * kTmaTile + px] = c[q];
-    }
-    __syncthreads();
-    if (!half && live) {
-#pragma unroll
-      for (int q = 1; q < NT; ++q) c[q] += xc[q * kTmaTile + px];
-      c[0] = (uint32_t)M;
-      a.lo[p] = lo;
-      a.hi[p] = hi;
-#pragma unroll
-      for (int b = 0; b < NT; ++b) {
-        const uint32_t v = flat ? 0u : (b + 1 < NT ? c[b] - c[b + 1] : c[b]);
-        if (a.wmode == CPB_WEIGHTS_U8)
-          static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
-        else
-          static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
-      }
-    }
-    __syncthreads();  // every thread is done with stage s and the exchange buffers
-    if (tid == 0) {
-      const int64_t tn = t + (int64_t)stages * gridDim.x;
-      if (tn < ntiles) issue(tn, s);
-    }
-    if (++s == stages) {
-      s = 0;
-      phase ^= 1u;
-    }
-  }
-  merge_range(vmin, vmax, bad, a.range);
-}
-
 template <int KIND, int NT>
 __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant__ CUtensorMap map,
                                                            FitArgs a, int stages, int mbox,
@@ -745,139 +629,6 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
   merge_range(vmin, vmax, bad, a.range);
 }
 
-// Split-role variant of the fused fit (used when moments AND bounds are
-// wanted): 2 x 128 threads per 128-pixel tile.  Threads [0, 128) run the
-// member-order float64 moment sums (FP64 pipe) and threads [128, 256) the
-// min / max and threshold binning (FP32 / integer pipes) of the same pixels
-// from the same staged tile; the roles need nothing from each other, so the
-// two instruction streams overlap on different pipes and the SM holds twice
-// the warps of the single-role kernel.  Same per-pixel arithmetic.
-template <int NT>
-__global__ void __launch_bounds__(2 * kTmaTile) fit_tma_multi2_kernel(
-    const __grid_constant__ CUtensorMap map, MultiArgs a, int stages, int mbox, int nbox,
-    int64_t ntiles) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int M = a.members;
-  const int rows = mbox * nbox;
-  const int tid = threadIdx.x;
-  const bool moment_role = tid < kTmaTile;
-  const int px = moment_role ? tid : tid - kTmaTile;
-  float* buf = reinterpret_cast<float*>(smem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)stages * rows * kTmaTile * 4);
-  if (tid == 0) {
-    prefetch_tensormap(&map);
-    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const uint64_t pol = policy_evict_first();
-  const uint32_t tile_bytes = (uint32_t)rows * kTmaTile * 4u;
-  auto issue = [&](int64_t tile, int s) {
-    mbar_arrive_expect_tx(&full[s], tile_bytes);
-    float* dst = buf + (size_t)s * rows * kTmaTile;
-    for (int b = 0; b < nbox; ++b)
-      tma_load_2d(dst + (size_t)b * mbox * kTmaTile, &map, (int)(tile * kTmaTile), b * mbox, &full[s], pol);
-  };
-  if (tid == 0) {
-    for (int k = 0; k < stages; ++k) {
-      const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
-      if (t < ntiles) issue(t, k);
-    }
-  }
-  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
-  bool bad = false;
-  int s = 0;           // ring slot of this tile
-  uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    mbar_wait(&full[s], phase);
-    const float* col = buf + (size_t)s * rows * kTmaTile + px;
-    const int64_t p = t * kTmaTile + px;
-    if (p < a.npix) {
-      if (moment_role) {
-        double sum = 0.0;
-#pragma unroll 8
-        for (int m = 0; m < M; ++m) sum = __dadd_rn(sum, (double)col[m * kTmaTile]);
-        const double mean = __ddiv_rn(sum, (double)M);
-        double sq = 0.0;
-#pragma unroll 8
-        for (int m = 0; m < M; ++m) {
-          const double d = __dsub_rn((double)col[m * kTmaTile], mean);
-          sq = __dadd_rn(sq, __dmul_rn(d, d));
-        }
-        const double sd = __dsqrt_rn(__ddiv_rn(sq, (double)(M - 1)));
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (a.mean[i]) {
-            a.mean[i][p] = mean;
-            a.spread[i][p] = sd;
-          }
-        }
-      } else {
-        float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
-#pragma unroll 8
-        for (int m = 0; m < M; ++m) {
-          const float x = col[m * kTmaTile];
-          lo = fmin_nan(lo, x);
-          hi = fmaxf(hi, x);
-        }
-        bad |= nonfinite(lo) | nonfinite(hi);
-        vmin = fminf(vmin, lo);
-        vmax = fmaxf(vmax, hi);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (a.lo[i]) {
-            a.lo[i][p] = lo;
-            a.hi[i][p] = hi;
-          }
-        }
-        if (NT > 0 && a.counts) {
-          constexpr int NB = NT > 0 ? NT : 1;
-          const double dlo = (double)lo;
-          const double scale = __ddiv_rn((double)a.bins, __dsub_rn((double)hi, dlo));
-          const float step = __fsub_rn(hi, lo) * __frcp_rn((float)a.bins);  // a guess: any rounding
-          uint32_t c[NB + 1];
-          float thr[NB];
-#pragma unroll
-          for (int q = 1; q < NB; ++q) {
-            thr[q] = hi > lo ? bin_threshold(q, dlo, scale, __fmaf_rn((float)q, step, lo), lo, hi) : 0.0f;
-            thr[q] = thr[q] == 0.0f ? -0.0f : thr[q];
-          }
-#pragma unroll
-          for (int q = 0; q <= NB; ++q) c[q] = 0u;
-#pragma unroll 4
-          for (int m = 0; m < M; ++m) {
-            const float x = col[m * kTmaTile];
-#pragma unroll
-            for (int q = 1; q < NB; ++q) c[q] += lt_bit(x, thr[q]);
-          }
-#pragma unroll
-          for (int q = 1; q < NB; ++q) c[q] = (uint32_t)M - c[q];
-          c[0] = (uint32_t)M;
-          const bool flat = !(hi > lo);
-#pragma unroll
-          for (int b = 0; b < NB; ++b) {
-            const uint32_t v = flat ? 0u : (b + 1 < NB ? c[b] - c[b + 1] : c[b]);
-            if (a.wmode == CPB_WEIGHTS_U8)
-              static_cast<uint8_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint8_t)v;
-            else
-              static_cast<uint16_t*>(a.counts)[(int64_t)b * a.wstride + p] = (uint16_t)v;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const int64_t tn = t + (int64_t)stages * gridDim.x;
-      if (tn < ntiles) issue(tn, s);
-    }
-    if (++s == stages) {
-      s = 0;
-      phase ^= 1u;
-    }
-  }
-  if (!moment_role) merge_range(vmin, vmax, bad, a.range);
-}
-
 __global__ void range_init_kernel(uint32_t* range) {
   range[0] = 0xffffffffu;
   range[1] = 0u;
@@ -1021,9 +772,8 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
     // ~32 KB of staging per CTA (one 64-member tile): more resident CTAs per SM
     // hide the TMA latency at least as well as a deeper per-CTA ring (histogram
     // 15.6 -> 13.2 ms, uniform unchanged at the HBM limit)
-    static const int stage_kb = [] { const char* e = getenv("CPB_FIT_STAGE_KB"); return e ? atoi(e) : 32; }();
-    static const int min_stages = [] { const char* e = getenv("CPB_FIT_MIN_STAGES"); return e ? atoi(e) : 1; }();
-    const int stages = (int)std::min<size_t>(8, std::max<size_t>(min_stages, ((size_t)stage_kb * 1024) / tile_bytes));
+    constexpr size_t kStageBytes = 32 * 1024;
+    const int stages = (int)std::min<size_t>(8, std::max<size_t>(1, kStageBytes / tile_bytes));
     const size_t smem = stages * tile_bytes + stages * 8 + cnt_bytes;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -1057,38 +807,15 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
     const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
     kern<<<(unsigned)grid, kTmaTile, smem, st>>>(map, c, stages, mbox, nbox, ntiles);            \
   } while (0)
-#define CPB_FIT_TMA_SPLIT(KERN)                                                                  \
-  do {                                                                                           \
-    auto kern = KERN;                                                                            \
-    const size_t sm2 = stages * tile_bytes + stages * 8 + (4 + kThreshBins) * kTmaTile * 4;      \
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);           \
-    int per_sm = 1;                                                                              \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * kTmaTile, sm2);             \
-    const int64_t grid = std::min<int64_t>(ntiles, (int64_t)sms * std::max(per_sm, 1));          \
-    kern<<<(unsigned)grid, 2 * kTmaTile, sm2, st>>>(map, c, stages, mbox, nbox, ntiles);         \
-  } while (0)
 #define CPB_FIT_TMA(K) \
   case K:              \
     CPB_FIT_TMA_LAUNCH((fit_tma_kernel<K, 0>)); \
     break;
-      static const int split = [] { const char* e = getenv("CPB_HIST_SPLIT"); return e ? atoi(e) : 0; }();
       switch (f->kind) {
         CPB_FIT_TMA(CPB_UNIFORM)
         CPB_FIT_TMA(CPB_EPANECHNIKOV)
         CPB_FIT_TMA(CPB_GAUSSIAN)
         case CPB_HISTOGRAM:
-          if (split && f->bins >= 2 && f->bins <= kThreshBins) {
-            switch (f->bins) {
-              case 2: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<2>)); break;
-              case 3: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<3>)); break;
-              case 4: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<4>)); break;
-              case 5: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<5>)); break;
-              case 6: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<6>)); break;
-              case 7: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<7>)); break;
-              default: CPB_FIT_TMA_SPLIT((fit_tma_hist2_kernel<8>)); break;
-            }
-            break;
-          }
           switch (f->bins <= kThreshBins ? f->bins : 0) {
             case 1: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 1>)); break;
             case 2: CPB_FIT_TMA_LAUNCH((fit_tma_kernel<CPB_HISTOGRAM, 2>)); break;
@@ -1106,7 +833,6 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
           return CPB_EINVAL;
       }
 #undef CPB_FIT_TMA_LAUNCH
-#undef CPB_FIT_TMA_SPLIT
 #undef CPB_FIT_TMA
       CPB_CHECK_LAUNCH("fit kernel (TMA)");
     }
@@ -1308,18 +1034,12 @@ int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, in
   }
   // one 32 KB stage per CTA (6-7 CTAs / SM): with the issue-bound fused passes,
   // more resident CTAs hide the TMA latency better than a deeper ring per CTA
-  // (19.7 vs 23.4 ms at config 5); CPB_FIT_MULTI_STAGES overrides
-  static const int mstages = [] { const char* e = getenv("CPB_FIT_MULTI_STAGES"); return e ? atoi(e) : 1; }();
-  const int stages = std::max(1, std::min(8, mstages));
+  // (19.7 vs 23.4 ms at config 5)
+  const int stages = 1;
   const size_t smem = stages * tile_bytes + stages * 8;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // split roles (CPB_FIT_SPLIT=1) when both the moment sums and the bounds / bins
-  // are wanted: 21.4 vs 23.4 ms alone, but it slows a concurrent stencil more
-  // (bench step 126.4 vs 124.7 ms overlapped), so it is off by default
-  static const int split_env = [] { const char* e = getenv("CPB_FIT_SPLIT"); return e ? atoi(e) : 0; }();
-  const bool split = split_env && (a.mean[0] || a.mean[1]) && (a.lo[0] || a.lo[1]);
   const int64_t max_chunk = (int64_t)1 << 30;
   for (int64_t p0 = 0; p0 < npix; p0 += max_chunk) {
     MultiArgs c = a;
@@ -1339,8 +1059,8 @@ int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, in
     const int64_t ntiles = (cn + kTmaTile - 1) / kTmaTile;
 #define CPB_MULTI(NTV)                                                                         \
   case NTV: {                                                                                  \
-    auto kern = split ? fit_tma_multi2_kernel<NTV> : fit_tma_multi_kernel<NTV>;                \
-    const int threads = split ? 2 * kTmaTile : kTmaTile;                                       \
+    auto kern = fit_tma_multi_kernel<NTV>;                                                     \
+    const int threads = kTmaTile;                                                              \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     int per_sm = 1;                                                                            \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);               \

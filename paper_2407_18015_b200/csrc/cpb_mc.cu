@@ -335,8 +335,9 @@ int launch_mc(const cpb_field* fld, int64_t row_begin, int64_t row_end, uint64_t
     set_error("sample counts must be positive");
     return CPB_EINVAL;
   }
-  if (n > 0x7fffffffll * 32) {
-    set_error("n_samples too large");
+  // per-vertex hit counts are uint32 (summed across the warp by __reduce_add_sync)
+  if (n > 0xffffffffll) {
+    set_error("n_samples too large (at most 2^32 - 1 per vertex)");
     return CPB_EINVAL;
   }
   McArgs a;

@@ -9,7 +9,8 @@ into G contiguous row slabs, one per rank (torchrun, NCCL over NVLink):
 2. one all-reduce (MAX over [-min, max]) gives the GLOBAL range, hence the
    same eps on every rank (distributions.py:30-36 is global, fields.py:136);
 3. one halo exchange sends the first / last owned row of every fitted plane
-   to the rank above / below (batched send/recv);
+   to the rank above / below, packed into one byte buffer per neighbour (one
+   send + one receive per neighbour per step, whatever the planes and bins);
 4. each rank runs the stencil (closed form or Monte Carlo) on its rows --
    Monte Carlo keys use GLOBAL pixel indices (engine.py:752-754), so the
    result is bit-identical for every G;
@@ -17,8 +18,11 @@ into G contiguous row slabs, one per rank (torchrun, NCCL over NVLink):
    E[#min], E[#max], E[#saddle] = sum over vertices of p.
 
 The helpers below (``slab_rows``, ``exchange_halo_rows``,
-``allreduce_range``, ``allreduce_sums``) are plain torch.distributed code so
-the multi-rank logic is tested on CPU with the gloo backend.
+``allreduce_range``, ``allreduce_sums``) are plain torch.distributed code.
+With NCCL they move device tensors directly; with gloo they stage device
+tensors through host copies, so the whole CUDA slab pipeline also runs as
+several processes sharing one GPU (tests/test_distributed_gpu.py) and the
+pure-host logic runs on CPU (tests/test_distributed_cpu.py).
 """
 
 from __future__ import annotations
@@ -68,7 +72,16 @@ class Slab:
 
 
 def slab_rows(height: int, rank: int, world: int) -> Slab:
-    """Contiguous, balanced row slabs (the first height % world ranks get one extra row)."""
+    """Contiguous, balanced row slabs (the first height % world ranks get one extra row).
+
+    Every rank must own at least two rows (one halo row is sent each way, and an
+    interior rank's first and last owned rows must differ from its halo rows),
+    so ``world`` may not exceed ``height // 2``.
+    """
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside world {world}")
+    if world > 1 and height < 2 * world:
+        raise ValueError(f"{height} rows cannot be split into {world} slabs of at least two rows")
     base, extra = divmod(height, world)
     r0 = rank * base + min(rank, extra)
     r1 = r0 + base + (1 if rank < extra else 0)
@@ -83,6 +96,26 @@ def _group_world(group):
     return dist.get_rank(group), dist.get_world_size(group)
 
 
+def _host_staged(t, group=None) -> bool:
+    """True when ``t`` lives on a GPU but the group's backend only moves host
+    tensors (gloo): the collective then runs on a host copy.  NCCL groups move
+    device tensors directly (over NVLink / NVSwitch)."""
+    import torch.distributed as dist
+
+    return t.is_cuda and dist.get_backend(group) == "gloo"
+
+
+def _all_reduce(t, op, group=None) -> None:
+    import torch.distributed as dist
+
+    if _host_staged(t, group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
 def allreduce_range(vmin: float, vmax: float, device, group=None) -> tuple[float, float]:
     """Global (min, max) over ranks: one MAX all-reduce of [-min, max]."""
     import torch
@@ -92,37 +125,75 @@ def allreduce_range(vmin: float, vmax: float, device, group=None) -> tuple[float
     if world == 1:
         return vmin, vmax
     t = torch.tensor([-vmin, vmax], dtype=torch.float64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    _all_reduce(t, dist.ReduceOp.MAX, group)
     return -float(t[0]), float(t[1])
+
+
+def _row_views(planes, row):
+    """Row ``row`` of every plane as byte views: (local_height, W) planes give a
+    (W,) row, (k, local_height, W) stacks a (k, W) block."""
+    import torch
+
+    out = []
+    for t in planes:
+        v = t[row] if t.dim() == 2 else t[:, row]
+        out.append(v)
+    return out
+
+
+def _pack(rows):
+    import torch
+
+    return torch.cat([r.contiguous().reshape(-1).view(torch.uint8) for r in rows])
+
+
+def _unpack(buf, rows) -> None:
+    off = 0
+    for r in rows:
+        n = r.numel() * r.element_size()
+        r.copy_(buf[off:off + n].view(r.dtype).view(r.shape))
+        off += n
 
 
 def exchange_halo_rows(planes, slab: Slab, group=None) -> None:
     """Fill the halo rows of every plane from the neighbouring ranks.
 
-    ``planes``: tensors shaped (local_height, W) or (k, local_height, W);
-    local row ``halo_top`` is the first owned row.  Sends the first owned row
-    up and the last owned row down, receives into row 0 / the last row.
+    ``planes``: tensors shaped (local_height, W) or (k, local_height, W), any
+    dtypes; local row ``halo_top`` is the first owned row.  The first owned row
+    of every plane goes up and the last one down, PACKED into one contiguous
+    byte buffer per neighbour (one send + one receive per neighbour, however
+    many planes and bins), and is unpacked into row 0 / the last row.
     """
+    import torch
     import torch.distributed as dist
 
     rank, world = _group_world(group)
-    if world == 1:
+    if world == 1 or not planes:
         return
-    ops = []
+    if slab.owned < 1:
+        raise ValueError("a rank with no rows cannot exchange halo rows")
     first = slab.halo_top
     last = slab.halo_top + slab.owned - 1
-    for t in planes:
-        views = [t] if t.dim() == 2 else [t[i] for i in range(t.shape[0])]
-        for v in views:
-            if slab.halo_top:
-                ops.append(dist.P2POp(dist.isend, v[first].contiguous(), rank - 1, group))
-                ops.append(dist.P2POp(dist.irecv, v[0], rank - 1, group))
-            if slab.halo_bottom:
-                ops.append(dist.P2POp(dist.isend, v[last].contiguous(), rank + 1, group))
-                ops.append(dist.P2POp(dist.irecv, v[last + 1], rank + 1, group))
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+    staged = _host_staged(planes[0], group)
+
+    def dev(t):
+        return t.cpu() if staged else t
+
+    ops, recv = [], []
+    if slab.halo_top:
+        send = dev(_pack(_row_views(planes, first)))
+        buf = torch.empty_like(send)
+        ops += [dist.P2POp(dist.isend, send, rank - 1, group), dist.P2POp(dist.irecv, buf, rank - 1, group)]
+        recv.append((buf, _row_views(planes, 0)))
+    if slab.halo_bottom:
+        send = dev(_pack(_row_views(planes, last)))
+        buf = torch.empty_like(send)
+        ops += [dist.P2POp(dist.isend, send, rank + 1, group), dist.P2POp(dist.irecv, buf, rank + 1, group)]
+        recv.append((buf, _row_views(planes, last + 1)))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    for buf, rows in recv:
+        _unpack(buf.to(planes[0].device) if staged else buf, rows)
 
 
 def allreduce_sums(sums, group=None):
@@ -131,7 +202,7 @@ def allreduce_sums(sums, group=None):
 
     _, world = _group_world(group)
     if world > 1:
-        dist.all_reduce(sums, op=dist.ReduceOp.SUM, group=group)
+        _all_reduce(sums, dist.ReduceOp.SUM, group)
     return sums
 
 
@@ -218,7 +289,7 @@ class SlabField:
             if world > 1:
                 import torch.distributed as dist
 
-                dist.all_reduce(self.pair, op=dist.ReduceOp.MAX, group=group)
+                _all_reduce(self.pair, dist.ReduceOp.MAX, group)
             _lib.check(lib.cpb_pair_to_eps(self.pair.data_ptr(), self.eps_t.data_ptr(), s))
         else:
             gmin, gmax = ctypes.c_double(), ctypes.c_double()
@@ -275,7 +346,7 @@ def finish_slab_fields(fields, group=None):
         if world > 1:
             import torch.distributed as dist
 
-            dist.all_reduce(f0.pair, op=dist.ReduceOp.MAX, group=group)
+            _all_reduce(f0.pair, dist.ReduceOp.MAX, group)
         for f in fields:
             _lib.check(lib.cpb_pair_to_eps(f0.pair.data_ptr(), f.eps_t.data_ptr(), s))
     else:
@@ -285,8 +356,8 @@ def finish_slab_fields(fields, group=None):
         gmin, gmax = allreduce_range(gmin.value, gmax.value, f0.pair.device, group)
         for f in fields:
             f.dev.eps = lib.cpb_epsilon(gmin, gmax)
-    for f in fields:
-        exchange_halo_rows(_plane_views(f.dev), f.slab, group)
+    # every field's boundary rows in ONE packed exchange per neighbour
+    exchange_halo_rows([v for f in fields for v in _plane_views(f.dev)], f0.slab, group)
 
 
 def fit_slab(ens_slab, model, slab: Slab, width: int, group=None, timer=None):

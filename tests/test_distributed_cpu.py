@@ -55,6 +55,10 @@ def _run(world, fn):
 def test_slab_rows_partition():
     for H in (3, 7, 64, 1000):
         for G in (1, 2, 3, 4, 8):
+            if G > 1 and H < 2 * G:  # every rank needs two rows
+                with pytest.raises(ValueError):
+                    slab_rows(H, 0, G)
+                continue
             slabs = [slab_rows(H, g, G) for g in range(G)]
             assert slabs[0].row_begin == 0 and slabs[-1].row_end == H
             for a, b in zip(slabs, slabs[1:]):

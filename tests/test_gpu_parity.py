@@ -410,6 +410,28 @@ def test_run_host_models_matches_oracle():
                                     o[0].ctypes.data, None, None, None))
 
 
+def test_run_host_partial_channels_and_per_member_copies(monkeypatch):
+    """Unrequested channels come back exactly 0.0 even with a non-NULL host plane
+    (test_engine.py:616-623), and the per-member H2D path (member planes wider
+    than the driver's maximum 2-D copy pitch) gives the same result."""
+    import ctypes
+
+    from paper_2407_18015_b200 import _lib
+
+    lib = _lib.load()
+    vals = np.ascontiguousarray(orc.ackley_ensemble(41, 57, 7, noise_amp=0.3, seed=4))
+    M, H, W = vals.shape
+    ref = orc.classify(orc.fit(vals, "uniform"), "uniform")
+    for pitch in (None, "64"):
+        if pitch:
+            monkeypatch.setenv("CPB_HOST_MAX_PITCH", pitch)
+        o = [np.full((H, W), np.nan) for _ in range(3)]
+        _lib.check(lib.cpb_run_host(vals.ctypes.data, M, H, W, 0, 5, 1.0, 0, 0, 0, _lib.CH_MIN,
+                                    o[0].ctypes.data, o[1].ctypes.data, o[2].ctypes.data, None))
+        assert np.max(np.abs(o[0] - ref["min"])) <= CLOSED_TOL
+        assert np.array_equal(o[1], np.zeros((H, W))) and np.array_equal(o[2], np.zeros((H, W)))
+
+
 # ---------------------------------------------------------------- combinatorial (Eq. 5)
 COMB_TOL = 1e-12  # the reference evaluates each all-uniform term exactly; we use 3-node GL
 
