@@ -11,25 +11,31 @@ all-reduce when N > 1.  value = (models x interior vertices) / step time.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 runs under torchrun as row slabs (strong scaling: the grid is fixed and
-split across ranks); the step time is the max over ranks.
+--gpus N > 1 runs N ranks (one per GPU, NCCL) as row slabs -- strong scaling:
+the grid is fixed and split across ranks; the step time is the max over
+ranks.  Without torchrun's environment, bench.py re-launches itself under
+torch.distributed.run (and fails if fewer than N GPUs are visible).
 
 Reported beside `value`:
-  e2e          same metric through the C ABI with HOST buffers
-               (cpb_run_host_models): every step copies the pinned host ensemble
-               in once (fitted for every model while resident) and every model's
-               three float64 planes out; N > 1 uses the slab pipeline with host
-               copies
+  e2e          the same metric through the public API with HOST buffers, every
+               step: (1) the C ABI, cpb_run_host_models (pinned host ensemble
+               in, every model's three float64 planes out), and (2) the Python
+               drop-in API -- EnsembleStack(numpy) + for each model
+               classify_field(UncertainField.from_ensemble(stack, model)) ->
+               numpy; timed over all K steps
   roofline     the dominant kernel's algorithmic bytes / its CUDA-event time
-               vs MEASURED_PEAKS.json hbm_gbs, plus the whole-step figure
-  cpu_baseline the numpy oracle (a restatement of the reference algorithm,
-               test infrastructure) on one host thread, on rows of the same
-               ensemble regenerated bit-identically on the host; the same rows
-               of the GPU result are checked against it (parity spot-check)
+               vs MEASURED_PEAKS.json hbm_gbs, the whole-step figure and the
+               FP64 pipe figures (ncu + the measured DFMA peak)
+  parity       the TIMED step's own output planes (all models) on 8 spread row
+               bands against the reference package (baseline/_ref) run on the
+               same float32 input bytes
+  cpu_baseline the reference's from_ensemble + classify_field on those bands
+               (host process pool, all cores), N = 1
   clocks       nvidia-smi SM clocks and throttle reasons sampled during the
                timed region
-`--impl reference` times the oracle port on all host cores (process pool),
-rank 0 only, on a bounded sample of the same workload.
+`--impl reference` times the reference package (baseline/_ref, its own
+workers= process pool over all host cores; the numpy oracle port when the
+install is missing) on a bounded row sample of the same workload, rank 0 only.
 """
 
 from __future__ import annotations
@@ -47,10 +53,12 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
 
 MODELS = ("uniform", "epanechnikov", "histogram")
 METRIC = "Mvertices/sec of min/max/saddle probability fields"
 PARAM_BYTES = {"uniform": 8, "epanechnikov": 16}  # compact params per pixel; histogram 8 + bins
+CHS = ("min", "max", "saddle")
 
 
 def param_bytes(kind, bins):
@@ -69,15 +77,11 @@ def parse():
     p.add_argument("--bins", type=int, default=5)
     p.add_argument("--models", default=",".join(MODELS))
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-cpu", action="store_true", help="no parity check / CPU baseline")
     p.add_argument("--serial", action="store_true", help="no fit/stencil overlap (one stream)")
     p.add_argument("--precision", choices=("fp64", "mixed"), default="fp64",
                    help="closed form: fp64 (reference parity ~1e-15) or mixed (FP32 GL evaluation "
                         "for uniform / Epanechnikov, stated bound 1e-6)")
-    p.add_argument("--fit-priority", choices=("high", "low"), default="high",
-                   help="stream priority of the (overlapped) fit relative to the stencils")
-    p.add_argument("--concurrent-stencils", action="store_true",
-                   help="run the models' stencils on separate streams (one output buffer each)")
     p.add_argument("--fit", choices=("fused", "separate"), default="fused",
                    help="fused: one cpb_fit_multi pass over the ensemble for all models per step; "
                         "separate: one cpb_fit per model")
@@ -94,6 +98,40 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def fp64_peak():
+    """Measured DFMA peak (tools/fp64_peak.cu on a B200, profiles/fp64_peak_r2.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r2.json")) as fh:
+            return float(json.load(fh)["dfma_tflops"]), "measured (tools/fp64_peak.cu)"
+    except Exception:
+        return 37.2, "nominal 148 SMs x 64 DFMA x 2 x 1.965 GHz"
+
+
+def reference_module():
+    """The reference package installed in baseline/_ref (tools/install_reference.sh), or None."""
+    if os.path.isdir(os.path.join(REF_PATH, "critprob")):
+        if REF_PATH not in sys.path:
+            sys.path.insert(1, REF_PATH)
+        try:
+            import critprob  # noqa: F401
+
+            return critprob
+        except Exception:
+            return None
+    return None
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 # ---------------------------------------------------------------------------
@@ -216,12 +254,15 @@ def run_ours(args):
     device = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
+        print(f"[bench] rank {rank}/{world}: NCCL process group on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
     H, W, M, bins = args.height, args.width, args.members, args.bins
     models = [m for m in args.models.split(",") if m]
     slab = D.slab_rows(H, rank, world)
     ens = cpb.synthetic_rows(slab.row_begin, slab.owned, W, H, M, noise_amp=0.3, seed=0)
     torch.cuda.synchronize()
-    out = torch.zeros((3, slab.local_height, W), dtype=torch.float64, device=device)
+    # one output set per model: the timed step keeps every model's planes (parity below)
+    outs = {k: torch.zeros((3, slab.local_height, W), dtype=torch.float64, device=device) for k in models}
     est = cpb.EstimatorSpec(precision=args.precision)
     timer = KernelTimer()
     sums = {}
@@ -230,86 +271,61 @@ def run_ours(args):
         from paper_2407_18015_b200 import _lib
 
         _lib.check(_lib.load().cpb_set_option(b"fit_ctas_per_sm", args.fit_ctas))
-    # stream priorities (lower = higher priority); --fit-priority low lets the
-    # stencils keep the SMs and the next step's fit fill the gaps
-    fit_hi = args.fit_priority == "high"
-    s_fit = torch.cuda.Stream(device=device, priority=-1 if fit_hi else 0)
-    s_cls = torch.cuda.Stream(device=device, priority=0 if fit_hi else -1)
+    # the fits (HBM / issue bound) on a high-priority stream run under the
+    # previous stencils (FP64 bound) on a low-priority one
+    s_fit = torch.cuda.Stream(device=device, priority=-1)
+    s_cls = torch.cuda.Stream(device=device, priority=0)
     fused = args.fit == "fused" and len(models) > 1
+    nsets = 2 if overlap else 1
     if fused:
         # all models fitted in ONE pass over the ensemble (cpb_fit_multi); two
-        # sets of halo-padded planes alternate between steps, so the next
-        # step's fit (HBM-bound, high-priority stream) runs under this step's
-        # stencils (FP64-bound, low-priority stream)
-        nsets = 2 if overlap else 1
+        # sets of halo-padded planes alternate between steps, so step k+1's fit
+        # runs under step k's stencils
         sets = [{k: D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models}
                 for _ in range(nsets)]
-        fitted = [torch.cuda.Event() for _ in range(nsets)]
-        consumed = [torch.cuda.Event() for _ in range(nsets)]
-        counter = [0]
-        conc = args.concurrent_stencils
-        if conc:
-            s_model = {k: torch.cuda.Stream(device=device, priority=0) for k in models}
-            outs = {k: torch.zeros((3, slab.local_height, W), dtype=torch.float64, device=device)
-                    for k in models}
+    else:
+        sets = [{k: D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models}]
+    fitted = [torch.cuda.Event() for _ in range(len(sets))]
+    consumed = [torch.cuda.Event() for _ in range(len(sets))]
+    counter = [0]
+    last = [0]
 
-        def step():
-            b = counter[0] % nsets
-            counter[0] += 1
-            fs = sets[b]
+    def step():
+        b = counter[0] % len(sets)
+        counter[0] += 1
+        last[0] = b
+        fs = sets[b]
+        if fused:
             timer.kind = "fused"
             with torch.cuda.stream(s_fit if overlap else torch.cuda.current_stream()):
                 if overlap:
                     s_fit.wait_event(consumed[b])
                 D.fit_slab_fields([fs[k] for k in models], ens, timer=timer)
                 fitted[b].record()
-            if conc:
-                # each model's stencil on its own stream: the load-latency-bound
-                # uniform and the FP64-bound stencils share the SMs
+            with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
+                if overlap:
+                    s_cls.wait_event(fitted[b])
                 for kind in models:
-                    sk = s_model[kind]
-                    sk.wait_event(fitted[b])
-                    with torch.cuda.stream(sk):
-                        timer.kind = kind
-                        _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=outs[kind],
-                                                        sums=True, timer=timer)
-                    s_cls.wait_stream(sk)
-                s_cls.record_event(consumed[b])
-            else:
-                with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
-                    if overlap:
-                        s_cls.wait_event(fitted[b])
-                    for kind in models:
-                        timer.kind = kind
-                        _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=out, sums=True,
-                                                        timer=timer)
-                    consumed[b].record()
-            if overlap or conc:
-                torch.cuda.current_stream().wait_stream(s_cls)
-    else:
-        # one reusable halo-padded field per model; eps stays on the device, so the
-        # fits (HBM-bound, high-priority stream) run ahead and overlap the previous
-        # model's stencil (FP64-bound, low-priority stream)
-        fields = {k: D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models}
-        fitted = {k: torch.cuda.Event() for k in models}
-        consumed = {k: torch.cuda.Event() for k in models}
-
-        def step():
+                    timer.kind = kind
+                    _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=outs[kind], sums=True,
+                                                    timer=timer)
+                consumed[b].record()
+        else:
             for kind in models:
                 timer.kind = kind
                 with torch.cuda.stream(s_fit if overlap else torch.cuda.current_stream()):
                     if overlap:
-                        s_fit.wait_event(consumed[kind])  # last step's stencil is done with the planes
-                    fields[kind].fit(ens, timer=timer)
-                    fitted[kind].record()
+                        s_fit.wait_event(consumed[b])
+                    fs[kind].fit(ens, timer=timer)
+                    fitted[b].record()
                 with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
                     if overlap:
-                        s_cls.wait_event(fitted[kind])
-                    _, sums[kind] = D.classify_slab(fields[kind].dev, slab, est, out=out, sums=True,
+                        s_cls.wait_event(fitted[b])
+                    _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=outs[kind], sums=True,
                                                     timer=timer)
-                    consumed[kind].record()
-            if overlap:
-                torch.cuda.current_stream().wait_stream(s_cls)
+                    consumed[b].record()
+        if overlap:
+            torch.cuda.current_stream().wait_stream(s_cls)
 
     def barrier():
         if world > 1:
@@ -343,9 +359,54 @@ def run_ours(args):
     verts = (H - 2) * (W - 2)
     value = len(models) * verts / (ms_step / 1e3) / 1e6
     expected = {k: [float(x) for x in v.cpu()] for k, v in sums.items()}
+    roofline = make_roofline(args, models, slab, per_kernel, ms_step)
+    hist = 1 if "histogram" in models else 0
+    if fused:  # range init, weight table, fused fit, range->pair, pair->eps per model, stencil + 2 count kernels per model
+        launches_per_step = 1 + hist + 1 + 1 + len(models) + 3 * len(models)
+    else:
+        launches_per_step = sum(5 + 2 + (1 if k == "histogram" else 0) for k in models)
 
-    # ---- roofline of the dominant kernel (this rank's launches)
+    # ---- parity of the timed step's own outputs + CPU baseline (rank 0)
+    cpu = parity = None
+    if rank == 0 and not args.no_cpu and not args.profile:
+        eps = {k: float(sets[last[0]][k].eps_t.item()) for k in models}
+        cpu, parity = parity_and_cpu_baseline(args, models, ens, outs, slab, eps, est,
+                                              with_baseline=(world == 1))
+    # ---- end to end through the public API with host buffers
+    del sets, outs, ens
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        e2e = run_e2e(args, models, slab, rank, world, device)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "Mvertices/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if args.precision == "fp64" else "f64 (histogram) / mixed f64-f32 (uniform, epanechnikov)",
+            "data": "synthetic (device-generated bowl + keyed-splitmix noise, host-reproducible)",
+            "config": {"workload": f"config5: {H}x{W} grid, {M} members, closed form, one step = "
+                                   f"fit + min/max/saddle for {'+'.join(models)} (bins={bins})",
+                       "height": H, "width": W, "members": M, "bins": bins, "models": models,
+                       "vertices_per_model": verts, "parallelism": f"row-slab x{world}",
+                       "fit": "one fused pass over the ensemble for all models" if fused else
+                              "one pass per model",
+                       "l2": f"inputs ({M * H * W * 4 / 1e9:.1f} GB ensemble) larger than L2; no flush needed"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
+            "clocks": clk, "gpu_launches": launches_per_step * args.steps,
+            "expected_counts": expected,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def make_roofline(args, models, slab, per_kernel, ms_step):
+    H, W, M, bins = args.height, args.width, args.members, args.bins
     hbm, peak_kind = peaks()
+    f64_peak, f64_kind = fp64_peak()
     owned_px = slab.owned * W
     a, b = slab.stencil_rows()
     st_verts = (b - a) * (W - 2)
@@ -372,7 +433,8 @@ def run_ours(args):
         except Exception:
             traffic = None
     # the stencils are FP64-bound: their pipe-level figures from the committed
-    # ncu capture (profiles/ncu_fp64.json, tools/ncu_fp64.py)
+    # ncu capture (profiles/ncu_fp64.json, tools/ncu_fp64.py), and the FLOP rate
+    # of THIS run's event time against the measured DFMA peak
     compute = None
     fpath = os.path.join(ROOT, "profiles", "ncu_fp64.json")
     if os.path.exists(fpath):
@@ -381,12 +443,16 @@ def run_ours(args):
             key = next((k for k in fp if k.split("<")[0] == dom["kernel"].split("<")[0]), None)
             if key:
                 r = fp[key]
-                compute = {"bound": "fp64", "kernel": key, "achieved": r["achieved_tflops"],
-                           "peak": r["peak_tflops"], "unit": "TFLOP/s", "frac": r["flop_frac"],
-                           "fp64_inst_frac": r["fp64_inst_frac"],
-                           "fp64_pipe_active_pct": r["fp64_pipe_active_pct"],
-                           "source": "ncu --set full (profiles/ncu_fp64.json); peak = ncu DFMA "
-                                     "peak_sustained x 2 x SM clock"}
+                flops = r["achieved_tflops"] * 1e12 * r["ms"] / 1e3  # per launch, from ncu
+                achieved = flops / (dom["ms"] / 1e3) / 1e12
+                compute = {"bound": "fp64", "kernel": key, "achieved": round(achieved, 2),
+                           "peak": f64_peak, "peak_source": f64_kind, "unit": "TFLOP/s",
+                           "frac": round(achieved / f64_peak, 4),
+                           "flop_per_launch": flops,
+                           "fp64_inst_frac_ncu": r["fp64_inst_frac"],
+                           "fp64_pipe_active_pct_ncu": r["fp64_pipe_active_pct"],
+                           "source": f"FLOP per launch from ncu --set full ({r.get('_report', 'profiles/ncu_fp64.json')}); "
+                                     "time = this run's CUDA events"}
         except Exception:
             compute = None
     # 4M + 24 bytes per vertex per model (the ensemble read once
@@ -395,115 +461,125 @@ def run_ours(args):
     step_bytes = len(models) * (owned_px * 4 * M + st_verts * 24)
     planes = sum(param_bytes(k, bins) for k in models)
     min_bytes = owned_px * (4 * M + planes) + st_verts * (planes + 24 * len(models))
-    roofline = {"bound": "hbm", "kernel": dom["kernel"], "achieved": round(dom["gbs"], 1),
-                "peak": hbm, "peak_source": peak_kind, "unit": "GB/s",
-                "frac": round(dom["gbs"] / hbm, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": dom["bytes"],
-                "step": {"bytes": step_bytes,
-                         "achieved": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
-                         "frac": round(step_bytes / (ms_step / 1e3) / 1e9 / hbm, 4),
-                         "note": "e2e algorithmic bytes 4M+24 per vertex per model (SURVEY 8d)",
-                         "fused_minimal_bytes": min_bytes,
-                         "fused_minimal_frac": round(min_bytes / (ms_step / 1e3) / 1e9 / hbm, 4)},
-                "kernels": {f"{k}/{w}": {"ms": round(r["ms"], 3), "GB/s": round(r["gbs"], 1)}
-                            for (k, w), r in kern.items()},
-                "compute": compute}
-    # our kernels per step: range init, fit(s), weight table (histogram),
-    # range->pair, pair->eps per field, one stencil per model and (closed form)
-    # the two expected-count reduction kernels per model
-    hist = 1 if "histogram" in models else 0
-    per_model_counts = 2 if est.method == "closed_form" else 0
-    if fused:
-        launches_per_step = 1 + 1 + hist + 1 + (2 + per_model_counts) * len(models)
+    return {"bound": "hbm", "kernel": dom["kernel"], "achieved": round(dom["gbs"], 1),
+            "peak": hbm, "peak_source": peak_kind, "unit": "GB/s",
+            "frac": round(dom["gbs"] / hbm, 4), "traffic": traffic,
+            "algorithmic_bytes_per_launch": dom["bytes"],
+            "step": {"bytes": step_bytes,
+                     "achieved": round(step_bytes / (ms_step / 1e3) / 1e9, 1),
+                     "frac": round(step_bytes / (ms_step / 1e3) / 1e9 / hbm, 4),
+                     "note": "e2e algorithmic bytes 4M+24 per vertex per model (SURVEY 8d)",
+                     "fused_minimal_bytes": min_bytes,
+                     "fused_minimal_frac": round(min_bytes / (ms_step / 1e3) / 1e9 / hbm, 4)},
+            "kernels": {f"{k}/{w}": {"ms": round(r["ms"], 3), "GB/s": round(r["gbs"], 1)}
+                        for (k, w), r in kern.items()},
+            "compute": compute}
+
+
+# ---------------------------------------------------------------------------
+# parity of the timed step + CPU baseline: the reference on host cores
+# ---------------------------------------------------------------------------
+def _pool_init(root, ref_path):
+    """Spawned worker: import paths only (the reference or the oracle port)."""
+    for p in (root, ref_path):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+
+def _ping(x):
+    return x
+
+
+def _band_task(task):
+    """One (row band, model) through the reference: from_ensemble + classify_field
+    (workers=1) on the band's float32 rows; returns its interior vertices."""
+    idx, rows, kind, bins, eps, use_ref = task
+    t = time.perf_counter()
+    if use_ref:
+        import critprob
+        import critprob.distributions as cdist
+
+        # eps is a property of the WHOLE ensemble (distributions.py:30-36); the band
+        # alone would give its own, so the reference helper returns the global one
+        cdist.default_epsilon = lambda values, _e=eps: _e
+        stack = critprob.EnsembleStack(rows)
+        field = critprob.UncertainField.from_ensemble(stack, critprob.ModelSpec(kind, bins=bins))
+        pf = critprob.classify_field(field, workers=1)
+        res = np.stack([pf.p_min, pf.p_max, pf.p_saddle])[:, 1:-1, 1:-1]
     else:
-        launches_per_step = sum(5 + per_model_counts + (1 if k == "histogram" else 0) for k in models)
+        from oracle import critprob_oracle as orc
 
-    # ---- parity spot-check + CPU baseline (rank 0, N = 1)
-    cpu = None
-    parity = None
-    if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
-        cpu, parity = cpu_baseline_and_parity(args, models, ens, out, est, slab)
-
-    # ---- end to end through the C ABI with host buffers
-    e2e = None
-    if not args.no_e2e and not args.profile:
-        del ens
-        torch.cuda.empty_cache()
-        e2e = run_e2e(args, models, slab, rank, world, device)
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "Mvertices/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64" if args.precision == "fp64" else "f64 (histogram) / mixed f64-f32 (uniform, epanechnikov)",
-            "data": "synthetic (device-generated bowl + keyed-splitmix noise, host-reproducible)",
-            "config": {"workload": f"config5: {H}x{W} grid, {M} members, closed form, one step = "
-                                   f"fit + min/max/saddle for {'+'.join(models)} (bins={bins})",
-                       "height": H, "width": W, "members": M, "bins": bins, "models": models,
-                       "vertices_per_model": verts, "parallelism": f"row-slab x{world}",
-                       "fit": "one fused pass over the ensemble for all models" if fused else
-                              "one pass per model",
-                       "l2": "inputs (68.7 GB ensemble) larger than L2; no flush needed"},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
-            "clocks": clk, "gpu_launches": launches_per_step * args.steps,
-            "expected_counts": expected,
-        }
-        print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+        ref = orc.classify(orc.fit(rows, kind, bins, eps=eps), kind)
+        res = np.stack([ref[c] for c in CHS])[:, 1:-1, 1:-1]
+    return idx, kind, res, time.perf_counter() - t
 
 
-def cpu_baseline_and_parity(args, models, ens, out_unused, est, slab):
-    # fp64: the reference's own grid-vs-case tolerance; mixed: the north_star's stated bound
+def parity_and_cpu_baseline(args, models, ens, outs, slab, eps, est, with_baseline=True,
+                            bands=8, band_rows=2):
+    """The timed step's own output planes (every model) on `bands` row bands
+    spread over this rank's slab vs the reference run on the same float32
+    input bytes, in a host process pool; the pool's throughput is the CPU
+    baseline (the reference on all host cores)."""
+    import multiprocessing as mp
+
+    H, W, bins = args.height, args.width, args.bins
+    crit = reference_module()
+    use_ref = crit is not None
     tol = 1e-12 if est.precision == "fp64" else 1e-6
-    """Oracle on rows [r0, r0+6) of the same ensemble (host twin), 1 thread; GPU rows compared."""
-    import torch
-
-    from oracle import critprob_oracle as orc
-    from paper_2407_18015_b200 import distributed as D
-
-    try:
-        from threadpoolctl import threadpool_limits
-        limit = threadpool_limits(1)
-    except Exception:  # pragma: no cover
-        limit = None
-    H, W, M, bins = args.height, args.width, args.members, args.bins
-    r0, nr = H // 2 - 3, 6
-    host = orc.synthetic_rows(r0, nr, W, H, M, noise_amp=0.3, seed=0)
-    dev_rows = ens[:, r0:r0 + nr].cpu().numpy()
-    bit_identical_input = bool(np.array_equal(host, dev_rows))
-    times, errs = {}, {}
-    verts = (nr - 2) * (W - 2)
-    out = torch.zeros((3, slab.local_height, W), dtype=torch.float64, device=ens.device)
-    for kind in models:
-        model_eps = None
-        dev = D.fit_slab(ens, __import__("paper_2407_18015_b200").ModelSpec(kind=kind, bins=bins), slab, W)
-        model_eps = dev.eps
-        D.classify_slab(dev, slab, est, out=out)
-        gpu = out[:, r0 + 1:r0 + nr - 1].cpu().numpy()
+    lo = max(slab.row_begin, 1)
+    hi = min(slab.row_end, H - 1)
+    starts = sorted({int(lo + 1 + (hi - lo - band_rows - 2) * (i + 0.5) / bands) for i in range(bands)})
+    tasks, gpu = [], {}
+    for i, g in enumerate(starts):  # vertex rows [g, g + band_rows), input rows [g - 1, g + band_rows + 1)
+        rows = ens[:, g - 1 - slab.row_begin:g + band_rows + 1 - slab.row_begin].cpu().numpy()
+        lg = g - slab.local_row0
+        for kind in models:
+            tasks.append((i, rows, kind, bins, eps[kind], use_ref))
+            gpu[(i, kind)] = outs[kind][:, lg:lg + band_rows, 1:W - 1].cpu().numpy()
+    cores = min(len(tasks), os.cpu_count() or 1)
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores, initializer=_pool_init, initargs=(ROOT, REF_PATH)) as pool:
+        pool.map(_ping, range(cores), chunksize=1)  # workers up before the clock
         t = time.perf_counter()
-        params = orc.fit(host, kind, bins, eps=model_eps)
-        ref = orc.classify(params, kind)
-        times[kind] = time.perf_counter() - t
-        errs[kind] = max(float(np.max(np.abs(gpu[i][:, 1:-1] - ref[ch][1:-1, 1:-1])))
-                         for i, ch in enumerate(("min", "max", "saddle")))
-    if limit is not None:
-        limit.unregister() if hasattr(limit, "unregister") else None
-    total = sum(times.values())
-    cpu = {"value": round(len(models) * verts / total / 1e6, 5), "unit": "Mvertices/s", "cores": 1,
-           "kind": "port",
-           "sample": f"rows [{r0},{r0 + nr}) of the config-5 ensemble ({verts} interior vertices "
-                     f"per model, all {len(models)} models), numpy oracle, 1 thread, fit+classify",
-           "seconds": {k: round(v, 3) for k, v in times.items()}}
-    parity = {"rows": [r0 + 1, r0 + nr - 1], "input_bit_identical": bit_identical_input,
-              "max_abs_err_vs_oracle": errs, "tolerance": tol,
-              "ok": bit_identical_input and all(e <= tol for e in errs.values())}
+        results = pool.map(_band_task, tasks, chunksize=1)
+        wall = time.perf_counter() - t
+    errs = {k: 0.0 for k in models}
+    secs = {k: 0.0 for k in models}
+    for i, kind, res, sec in results:
+        errs[kind] = max(errs[kind], float(np.max(np.abs(gpu[(i, kind)] - res))))
+        secs[kind] += sec
+    nv = band_rows * (W - 2)
+    parity = {"rows": [[g, g + band_rows] for g in starts], "models": models,
+              "what": "the timed step's own output planes (last step, every model)",
+              "against": "reference package (baseline/_ref critprob: from_ensemble + classify_field)"
+                         if use_ref else "numpy oracle port (baseline/_ref missing)",
+              "input": "the same float32 rows, read back from the device ensemble",
+              "eps": "global eps of the whole ensemble (the fit's device pair)",
+              "max_abs_err": errs, "tolerance": tol,
+              "ok": all(e <= tol for e in errs.values())}
+    cpu = None
+    if with_baseline:
+        total_v = len(starts) * nv * len(models)
+        cpu = {"value": round(total_v / wall / 1e6, 5), "unit": "Mvertices/s", "cores": cores,
+               "kind": "reference" if use_ref else "port",
+               "single_process_value": round(total_v / sum(secs.values()) / 1e6, 5),
+               "host_cpu": cpu_model(), "host_cpus_visible": os.cpu_count(),
+               "sample": f"{len(starts)} bands x {band_rows} vertex rows x {W - 2} columns of the config-5 "
+                         f"ensemble, {'+'.join(models)}: the reference's from_ensemble + classify_field "
+                         f"(workers=1) per (band, model), {cores} host processes",
+               "seconds_per_model_single_process": {k: round(v, 2) for k, v in secs.items()}}
     return cpu, parity
 
 
+# ---------------------------------------------------------------------------
+# end to end: host buffers through the public API
+# ---------------------------------------------------------------------------
 def run_e2e(args, models, slab, rank, world, device):
-    """Same metric through host buffers: H2D of the ensemble + fit + classify + D2H, every step."""
+    """Same metric through host buffers, every step: H2D of the ensemble + fits +
+    stencils + D2H of every model's planes.  N = 1: the C ABI
+    (cpb_run_host_models, pinned buffers) and the Python drop-in API (numpy in /
+    numpy out); N > 1: each rank's slab pipeline with pinned copies."""
     import torch
 
     import paper_2407_18015_b200 as cpb
@@ -512,70 +588,83 @@ def run_e2e(args, models, slab, rank, world, device):
 
     H, W, M, bins = args.height, args.width, args.members, args.bins
     lib = _lib.load()
-    steps = max(1, min(args.steps, 2))
+    steps = max(1, args.steps)
+    nm = len(models)
+    verts = (H - 2) * (W - 2)
     if world == 1:
-        n_ens = M * H * W
-        p_ens = ctypes.c_void_p()
-        p_out = ctypes.c_void_p()
-        nm = len(models)
-        _lib.check(lib.cpb_host_alloc(ctypes.byref(p_ens), n_ens * 4))
-        _lib.check(lib.cpb_host_alloc(ctypes.byref(p_out), nm * 3 * H * W * 8 + H * W))
-        try:
-            host = np.ctypeslib.as_array((ctypes.c_float * n_ens).from_address(p_ens.value))
-            host = host.reshape(M, H, W)
-            chunk = max(1, (1 << 30) // (M * W * 4))
-            for r in range(0, H, chunk):  # fill from the device generator, untimed
-                n = min(chunk, H - r)
-                host[:, r:r + n] = cpb.synthetic_rows(r, n, W, H, M).cpu().numpy()
-            outs = (ctypes.c_void_p * (3 * nm))(*[p_out.value + q * H * W * 8 for q in range(3 * nm)])
-            valid = p_out.value + 3 * nm * H * W * 8
-            kinds = (ctypes.c_int32 * nm)(*[_lib.KIND_CODES[k] for k in models])
-            binsv = (ctypes.c_int32 * nm)(*([bins] * nm))
-            ks = (ctypes.c_double * nm)(*[float(cpb.ModelSpec(k).k) for k in models])
+        host = cpb.pinned_empty((M, H, W), np.float32)  # the user's ensemble, page-locked
+        chunk = max(1, (1 << 30) // (M * W * 4))
+        for r in range(0, H, chunk):  # fill from the device generator, untimed
+            n = min(chunk, H - r)
+            host[:, r:r + n] = cpb.synthetic_rows(r, n, W, H, M).cpu().numpy()
+        outbuf = cpb.pinned_empty((nm, 3, H, W), np.float64)
+        valid = np.empty((H, W), np.uint8)
+        outs = (ctypes.c_void_p * (3 * nm))(*[outbuf[i, c].ctypes.data for i in range(nm) for c in range(3)])
+        kinds = (ctypes.c_int32 * nm)(*[_lib.KIND_CODES[k] for k in models])
+        binsv = (ctypes.c_int32 * nm)(*([bins] * nm))
+        ks = (ctypes.c_double * nm)(*[float(cpb.ModelSpec(k).k) for k in models])
 
-            def one():  # the reference workflow: one stack, every model (one upload)
-                _lib.check(lib.cpb_run_host_models(p_ens.value, M, H, W, nm, kinds, binsv, ks, 0, 0,
-                                                   0, 7, outs, valid))
-            one()  # warm-up (pools, module load)
-            t = time.perf_counter()
-            for _ in range(steps):
-                one()
-            sec = (time.perf_counter() - t) / steps
-            # raw pinned H2D bandwidth of this host, for context
-            dev_buf = torch.empty(1 << 28, dtype=torch.float32, device=device)
-            hb = torch.from_numpy(host.reshape(-1)[: 1 << 28])
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            dev_buf.copy_(hb, non_blocking=True)
-            torch.cuda.synchronize()
-            h2d_gbs = (1 << 30) / (time.perf_counter() - t) / 1e9
-            del dev_buf
-        finally:
-            lib.cpb_host_free(p_ens)
-            lib.cpb_host_free(p_out)
-        verts = (H - 2) * (W - 2)
+        def capi():  # the reference workflow: one stack, every model (one upload)
+            _lib.check(lib.cpb_run_host_models(host.ctypes.data, M, H, W, nm, kinds, binsv, ks, 0, 0,
+                                               0, 7, outs, valid.ctypes.data))
+        capi()  # warm-up (pools, module load)
+        t = time.perf_counter()
+        for _ in range(steps):
+            capi()
+        sec = (time.perf_counter() - t) / steps
+        lib.cpb_release_workspace(None)
+        # the Python drop-in API, numpy in / numpy out, exactly the reference's calls
+        mspecs = [cpb.ModelSpec(k, bins=bins) for k in models]
+
+        def python_api():
+            stack = cpb.EnsembleStack(host)  # one upload (+ the NaN/Inf check) per step
+            res = [cpb.classify_field(cpb.UncertainField.from_ensemble(stack, m)) for m in mspecs]
+            return res
+        python_api()
+        torch.cuda.empty_cache()
+        t = time.perf_counter()
+        for _ in range(steps):
+            res = python_api()
+            del res
+        sec_py = (time.perf_counter() - t) / steps
+        # raw pinned H2D bandwidth of this host, for context
+        dev_buf = torch.empty(1 << 28, dtype=torch.float32, device=device)
+        hb = torch.from_numpy(host.reshape(-1)[: 1 << 28])
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        dev_buf.copy_(hb, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_gbs = (1 << 30) / (time.perf_counter() - t) / 1e9
+        del dev_buf, host, outbuf
         return {"value": round(nm * verts / sec / 1e6, 2), "unit": "Mvertices/s",
-                "h2d_bytes_per_step": n_ens * 4,
-                "d2h_bytes_per_step": nm * (3 * H * W * 8),
+                "h2d_bytes_per_step": M * H * W * 4,
+                "d2h_bytes_per_step": nm * 3 * H * W * 8,
                 "steps": steps, "ms_per_step": round(sec * 1e3, 1),
                 "host_h2d_gbs": round(h2d_gbs, 1),
                 "path": "cpb_run_host_models (C ABI, pinned host buffers; the ensemble crosses "
-                        "PCIe once per step and is fitted for all models while resident)"}
+                        "PCIe once per step and is fitted for all models while resident)",
+                "python_api": {"value": round(nm * verts / sec_py / 1e6, 2), "unit": "Mvertices/s",
+                               "ms_per_step": round(sec_py * 1e3, 1), "steps": steps,
+                               "h2d_bytes_per_step": M * H * W * 4,
+                               "d2h_bytes_per_step": nm * 3 * H * W * 8,
+                               "path": "EnsembleStack(numpy, pinned) + for each model classify_field("
+                                       "UncertainField.from_ensemble(stack, model)) -> numpy planes"}}
     # N > 1: per-rank slab pipeline with host copies
     import torch.distributed as dist
 
     host = torch.empty((M, slab.owned, W), dtype=torch.float32).pin_memory()
     host.copy_(cpb.synthetic_rows(slab.row_begin, slab.owned, W, H, M))
-    res = torch.empty((3, slab.local_height, W), dtype=torch.float64).pin_memory()
+    res = torch.empty((nm, 3, slab.local_height, W), dtype=torch.float64).pin_memory()
     est = cpb.EstimatorSpec()
+    fields = [D.SlabField(cpb.ModelSpec(kind=k, bins=bins), slab, W, M, device) for k in models]
 
-    def one():  # one upload of the slab per step, every model fitted from it
+    def one():  # one upload of the slab per step, every model fitted from it in one pass
         ens = host.to(device, non_blocking=True)
-        for kind in models:
-            dev = D.fit_slab(ens, cpb.ModelSpec(kind=kind, bins=bins), slab, W)
-            out, _ = D.classify_slab(dev, slab, est, sums=True)
-            res.copy_(out, non_blocking=True)
-            torch.cuda.synchronize()
+        D.fit_slab_fields(fields, ens)
+        for i, f in enumerate(fields):
+            out, _ = D.classify_slab(f.dev, slab, est, sums=True)
+            res[i].copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
     one()
     dist.barrier()
     t = time.perf_counter()
@@ -584,76 +673,77 @@ def run_e2e(args, models, slab, rank, world, device):
     dist.barrier()
     sec = torch.tensor([(time.perf_counter() - t) / steps], dtype=torch.float64, device=device)
     dist.all_reduce(sec, op=dist.ReduceOp.MAX)
-    verts = (H - 2) * (W - 2)
-    return {"value": round(len(models) * verts / float(sec[0]) / 1e6, 2), "unit": "Mvertices/s",
+    return {"value": round(nm * verts / float(sec[0]) / 1e6, 2), "unit": "Mvertices/s",
             "h2d_bytes_per_step": M * H * W * 4,
-            "d2h_bytes_per_step": len(models) * 3 * H * W * 8, "steps": steps,
-            "path": "row-slab pipeline with pinned host copies per rank"}
+            "d2h_bytes_per_step": nm * 3 * H * W * 8, "steps": steps,
+            "path": "row-slab pipeline per rank: pinned slab H2D, fused fit, NCCL eps + halo, "
+                    "stencils, pinned D2H (max over ranks)"}
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the oracle port on all host cores
+# reference arm: the reference package on all host cores
 # ---------------------------------------------------------------------------
-_CACHE = {}
-
-
-def _ref_init(counter, W, H, M, rows, stride):
-    """Pool initializer: each worker regenerates its own row slab once (untimed)."""
+def _synth_band(r0, nrows, W, H, M):
+    """Rows [r0, r0 + nrows) of the config-5 ensemble on the host (the bit-identical
+    host twin of the device generator; test infrastructure, used as input only)."""
     from oracle import critprob_oracle as orc
 
-    with counter.get_lock():
-        wid = counter.value
-        counter.value += 1
-    r0 = min(wid * stride, H - rows - 2)
-    _CACHE["slab"] = orc.synthetic_rows(r0, rows + 2, W, H, M, noise_amp=0.3, seed=0)
-
-
-def _ref_work(task):
-    from oracle import critprob_oracle as orc
-
-    models, bins, eps = task
-    slab = _CACHE["slab"]
-    n = 0
-    for kind in models:
-        ref = orc.classify(orc.fit(slab, kind, bins, eps=eps), kind)
-        n += (slab.shape[1] - 2) * (slab.shape[2] - 2)
-        assert ref["min"].shape == slab.shape[1:]
-    return n
+    return orc.synthetic_rows(r0, nrows, W, H, M, noise_amp=0.3, seed=0)
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
-
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
     H, W, M, bins = args.height, args.width, args.members, args.bins
     models = [m for m in args.models.split(",") if m]
     cores = os.cpu_count() or 1
-    total_steps = args.steps + args.warmup
-    rows = 4 if total_steps <= 10 else (2 if total_steps <= 20 else 1)
-    # eps of the full ensemble (distributions.py:30-36): the bowl spans [0, 5] and the noise
-    # +-0.3; eps only affects degenerate pixels, of which the synthetic ensemble has none
+    crit = reference_module()
+    # a bounded sample: enough vertex rows to give every worker of the reference's own
+    # pool (classify_field(workers=cores), 4096-pixel chunks, engine.py:757-779) a chunk
+    vrows = max(2, min(64, -(-cores * 4096 // (W - 2))))
+    r0 = H // 2 - vrows // 2 - 1
+    band = _synth_band(r0, vrows + 2, W, H, M)
+    # eps of the full ensemble (distributions.py:30-36): the bowl spans [0, 5] and the
+    # noise +-0.3, so its range is [-0.3, 5.3] to float rounding; eps only affects
+    # degenerate pixels, of which the noisy synthetic ensemble has none
     eps = max(1e-12, 1e-9 * (5.3 - (-0.3)))
-    stride = max(rows + 2, (H - 2) // cores)
-    ctx = mp.get_context("fork")
-    counter = ctx.Value("i", 0)
-    with ctx.Pool(cores, initializer=_ref_init, initargs=(counter, W, H, M, rows, stride)) as pool:
-        work = [(models, bins, eps)] * cores
-        for _ in range(args.warmup):
-            pool.map(_ref_work, work, chunksize=1)
-        t = time.perf_counter()
-        done = 0
-        for _ in range(args.steps):
-            done += sum(pool.map(_ref_work, work, chunksize=1))
-        sec = time.perf_counter() - t
-    value = done / sec / 1e6
-    sample = (f"{cores} worker processes x {rows} interior rows x {W - 2} columns of the config-5 "
-              f"ensemble ({M} members) per step, fit + closed form for {'+'.join(models)}")
+    nv = vrows * (W - 2)
+    if crit is not None:
+        import critprob.distributions as cdist
+
+        cdist.default_epsilon = lambda values: eps
+        specs = [crit.ModelSpec(k, bins=bins) for k in models]
+
+        def one():
+            stack = crit.EnsembleStack(band)
+            for m in specs:
+                crit.classify_field(crit.UncertainField.from_ensemble(stack, m), workers=cores)
+        kind = "reference"
+        how = (f"the reference package (baseline/_ref critprob): EnsembleStack + from_ensemble + "
+               f"classify_field(workers={cores}) -- its own process pool")
+    else:
+        from oracle import critprob_oracle as orc
+
+        def one():
+            for k in models:
+                orc.classify(orc.fit(band, k, bins, eps=eps), k)
+        kind = "port"
+        how = "numpy oracle port, 1 process (baseline/_ref missing)"
+    for _ in range(args.warmup):
+        one()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    sec = time.perf_counter() - t
+    value = len(models) * nv * args.steps / sec / 1e6
+    sample = (f"{vrows} vertex rows x {W - 2} columns of the config-5 ensemble ({M} members) per step, "
+              f"fit + closed form for {'+'.join(models)}; {how}")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "Mvertices/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": args.gpus, "host_cores": cores,
+            "device": "host CPU only (n_gpus echoes --gpus; no GPU is used by this arm)", "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(sec / args.steps * 1e3, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (host twin of the device generator)",
@@ -661,19 +751,44 @@ def run_reference(args):
                                    f"{'+'.join(models)} (bins={bins}) -- bounded row sample",
                        "height": H, "width": W, "members": M, "bins": bins, "models": models},
             "cpu_baseline": {"value": round(value, 5), "unit": "Mvertices/s", "cores": cores,
-                             "kind": "port", "sample": sample},
+                             "kind": kind, "sample": sample, "host_cpu": cpu_model()},
             "e2e": {"value": round(value, 5), "unit": "Mvertices/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
-    print(json.dumps(line))
+    print(json.dumps(line), flush=True)
+
+
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run N ranks under torch.distributed.run."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return 0
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and int(os.environ.get("RANK", "0")) == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE={world}; running {world} ranks",
+              file=sys.stderr)
+    run_ours(args)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -173,6 +173,11 @@ int cpb_pair_to_eps(const double* d_pair, double* d_eps, void* stream);
 int cpb_fit_multi(const float* d_ens, int64_t member_stride, cpb_field* const* fields,
                   int32_t n_fields, uint32_t* d_range, int32_t accumulate, void* stream);
 
+/* Synchronous finiteness check of n device floats (EnsembleStack's
+ * isfinite validation, fields.py:54-55, run in HBM instead of on the host):
+ * CPB_ENONFINITE if any value is NaN or +-Inf. */
+int cpb_check_finite(const float* d_values, int64_t n, void* stream);
+
 /* Synchronously read back a d_range written by cpb_fit; returns
  * CPB_ENONFINITE if any value was NaN/Inf. */
 int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* stream);

@@ -51,6 +51,7 @@ from .fields import (
     ModelSpec,
     ProbabilityField,
     UncertainField,
+    pinned_empty,
     set_device,
 )
 from .field_io import (
@@ -73,7 +74,7 @@ from .synth import synthetic_ensemble, synthetic_rows
 __all__ = [
     "CHANNELS", "COMBINATORIAL_MAX_BINS", "ESTIMATOR_METHODS", "MODEL_KINDS", "PATTERNS",
     "EnsembleStack", "EstimatorSpec", "ModelSpec", "ProbabilityField", "UncertainField",
-    "classify_field", "pixel_index", "set_device", "synthetic_ensemble", "synthetic_rows",
+    "classify_field", "pinned_empty", "pixel_index", "set_device", "synthetic_ensemble", "synthetic_rows",
     "unit_block", "unit_planes", "UcvfError", "UcvfFormatError", "UcvfPayloadError",
     "UcvfValueError", "export_heatmap", "load_ensemble", "load_probability_field",
     "load_scalar_field", "save_ensemble", "save_probability_field", "save_scalar_field",

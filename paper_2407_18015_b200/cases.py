@@ -319,10 +319,12 @@ def pack_arrays(cases):
     w = np.zeros((n, P, maxb))
     for i, c in enumerate(cases):
         for p, d in enumerate((c.center, *c.neighbors)):
-            if isinstance(d, GaussianSampler):
+            # duck-typed, so the reference's own distribution objects pack too
+            # (integration.patch_reference)
+            if not hasattr(d, "support") and hasattr(d, "stddev"):  # GaussianSampler
                 kind[i, p], a[i, p], b[i, p] = 3, d.mean, d.stddev
                 continue
-            if not isinstance(d, FiniteDistribution):
+            if getattr(d, "kind", None) not in _KINDS or not hasattr(d, "support"):
                 raise TypeError(f"unsupported distribution {type(d).__name__}")
             kind[i, p] = _lib.KIND_CODES[d.kind]
             a[i, p], b[i, p] = d.support.lo, d.support.hi

@@ -20,6 +20,7 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
 int launch_from_scalar(const double* v, int64_t n, double half, double* lo, double* hi,
                        cudaStream_t st);
 int launch_range_to_pair(const uint32_t* range, double* pair, cudaStream_t st);
+int launch_nonfinite(const float* v, int64_t n, uint32_t* flag, cudaStream_t st);
 int launch_pair_to_eps(const double* pair, double* eps, cudaStream_t st);
 int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cudaStream_t st);
 int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
@@ -47,6 +48,8 @@ int launch_cases_semi(const cpb_case_batch* b, uint64_t seed, const uint64_t* pi
 int launch_cases_combinatorial(const cpb_case_batch* b, double* out, cudaStream_t st);
 
 extern int g_fit_ctas_per_sm;
+int workspace_alloc(void** p, size_t bytes, cudaStream_t st);
+void workspace_free(void* p, cudaStream_t st);
 
 static thread_local char g_err[512] = "";
 
@@ -196,6 +199,24 @@ int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* st
   if (gmin) *gmin = (double)ordered_to_float(h[0]);
   if (gmax) *gmax = (double)ordered_to_float(h[1]);
   return CPB_OK;
+}
+
+int cpb_check_finite(const float* d_values, int64_t n, void* stream) {
+  if (n < 0 || (n > 0 && !d_values)) { set_error("invalid values"); return CPB_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* flag = nullptr;
+  if (int rc = workspace_alloc((void**)&flag, sizeof(uint32_t), st)) return rc;
+  uint32_t h = 0;
+  cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(uint32_t), st);
+  int rc = e == cudaSuccess ? launch_nonfinite(d_values, n, flag, st) : cuda_status(e, "memset");
+  if (rc == CPB_OK) {
+    e = cudaMemcpyAsync(&h, flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = cuda_status(e, "finiteness flag");
+  }
+  workspace_free(flag, st);
+  if (rc == CPB_OK && h) { set_error("ensemble values must be finite"); return CPB_ENONFINITE; }
+  return rc;
 }
 
 int cpb_range_to_pair(const uint32_t* d_range, double* d_pair, void* stream) {

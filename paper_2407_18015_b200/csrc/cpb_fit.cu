@@ -629,6 +629,25 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
   merge_range(vmin, vmax, bad, a.range);
 }
 
+// any non-finite value in n floats -> *flag = 1 (float4 loads; exponent all ones)
+__global__ void nonfinite_kernel(const float* v, int64_t n, uint32_t* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned bad = 0;
+  const int64_t n4 = ((reinterpret_cast<uintptr_t>(v) & 15) == 0) ? n / 4 : 0;
+  const float4* v4 = reinterpret_cast<const float4*>(v);
+  for (int64_t i = t; i < n4; i += stride) {
+    const float4 x = __ldcs(v4 + i);
+    bad |= ((__float_as_uint(x.x) & 0x7f800000u) == 0x7f800000u) |
+           ((__float_as_uint(x.y) & 0x7f800000u) == 0x7f800000u) |
+           ((__float_as_uint(x.z) & 0x7f800000u) == 0x7f800000u) |
+           ((__float_as_uint(x.w) & 0x7f800000u) == 0x7f800000u);
+  }
+  for (int64_t i = 4 * n4 + t; i < n; i += stride)
+    bad |= (__float_as_uint(v[i]) & 0x7f800000u) == 0x7f800000u;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *flag = 1u;
+}
+
 __global__ void range_init_kernel(uint32_t* range) {
   range[0] = 0xffffffffu;
   range[1] = 0u;
@@ -870,6 +889,18 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
   }
 #undef CPB_FIT_CASE
   CPB_CHECK_LAUNCH("fit kernel");
+  return CPB_OK;
+}
+
+int launch_nonfinite(const float* v, int64_t n, uint32_t* flag, cudaStream_t st) {
+  if (n <= 0) return CPB_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n / 4 + 255) / 256;
+  nonfinite_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * 8)), 256, 0, st>>>(
+      v, n, flag);
+  CPB_CHECK_LAUNCH("finiteness check");
   return CPB_OK;
 }
 

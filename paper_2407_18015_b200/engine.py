@@ -163,7 +163,7 @@ def classify_field(
     valid[1:-1, 1:-1] = True
     if output == "device":
         return ProbabilityField(planes[0], planes[1], planes[2], valid)
-    host = planes.cpu().numpy()
+    host = planes.cpu().numpy()  # one D2H; the channels are views of it (no host copies)
     mask = np.zeros((H, W), dtype=bool)
     mask[1:-1, 1:-1] = True
-    return ProbabilityField(host[0].copy(), host[1].copy(), host[2].copy(), mask)
+    return ProbabilityField(host[0], host[1], host[2], mask)

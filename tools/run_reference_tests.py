@@ -1,0 +1,67 @@
+"""Run the reference's UNMODIFIED test files against the GPU path.
+
+    python tools/run_reference_tests.py [pytest args...]   (GPU box; needs baseline/_ref,
+                                                          see tools/install_reference.sh)
+
+The reference package (baseline/_ref/critprob) is imported, its hot-path
+entry points are swapped for the sm_100a path by
+paper_2407_18015_b200.integration.patch_reference (before any test module
+binds them), and pytest runs the reference's own test files
+(baseline/_ref/critprob_tests).  Writes a JSON summary to
+gpurun_out/reference_tests.json.
+"""
+
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+sys.path.insert(0, ROOT)
+sys.path.insert(0, REF)
+
+import pytest  # noqa: E402
+
+
+class _Patch:
+    """pytest plugin: patch before collection, count outcomes."""
+
+    def __init__(self):
+        self.outcomes = {}
+        self.failed = []
+
+    def pytest_configure(self, config):
+        import critprob
+
+        from paper_2407_18015_b200.integration import patch_reference
+
+        self.swapped = sorted(patch_reference(critprob))
+
+    def pytest_runtest_logreport(self, report):
+        if report.when == "call" or (report.when == "setup" and report.outcome != "passed"):
+            self.outcomes[report.outcome] = self.outcomes.get(report.outcome, 0) + 1
+            if report.outcome == "failed":
+                self.failed.append(report.nodeid)
+
+
+def main():
+    files = [os.path.join(REF, "critprob_tests", f) for f in
+             ("test_engine.py", "test_fields.py", "test_acceptance.py", "test_bench.py",
+              "test_field_io.py", "test_cli.py")]
+    plugin = _Patch()
+    t = time.time()
+    rc = pytest.main(["-q", "-p", "no:cacheprovider", "--rootdir", REF, *files, *sys.argv[1:]],
+                     plugins=[plugin])
+    out = {"rc": int(rc), "seconds": round(time.time() - t, 1), "outcomes": plugin.outcomes,
+           "failed": plugin.failed, "swapped": getattr(plugin, "swapped", []),
+           "files": [os.path.basename(f) for f in files]}
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    with open(os.path.join(ROOT, "gpurun_out", "reference_tests.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+    print(json.dumps(out))
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())
