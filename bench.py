@@ -276,8 +276,12 @@ def run_ours(args):
     s_fit = torch.cuda.Stream(device=device, priority=-1)
     s_cls = torch.cuda.Stream(device=device, priority=0)
     fused = args.fit == "fused" and len(models) > 1
+    # a uniform-only step is ONE kernel: fit and stencil fused (cpb_fit_classify)
+    fuse_uniform = models == ["uniform"] and args.fit == "fused" and args.precision == "fp64"
     nsets = 2 if overlap else 1
-    if fused:
+    if fuse_uniform:
+        sets = [{"uniform": D.SlabField(cpb.ModelSpec("uniform"), slab, W, M, device)}]
+    elif fused:
         # all models fitted in ONE pass over the ensemble (cpb_fit_multi); two
         # sets of halo-padded planes alternate between steps, so step k+1's fit
         # runs under step k's stencils
@@ -289,12 +293,18 @@ def run_ours(args):
     consumed = [torch.cuda.Event() for _ in range(len(sets))]
     counter = [0]
     last = [0]
+    work = [None]
 
     def step():
         b = counter[0] % len(sets)
         counter[0] += 1
         last[0] = b
         fs = sets[b]
+        if fuse_uniform:
+            timer.kind = "uniform"
+            sums["uniform"], work[0] = D.fit_classify_uniform(fs["uniform"], ens, slab, outs["uniform"],
+                                                              timer=timer, work=work[0])
+            return
         if fused:
             timer.kind = "fused"
             with torch.cuda.stream(s_fit if overlap else torch.cuda.current_stream()):
@@ -361,7 +371,9 @@ def run_ours(args):
     expected = {k: [float(x) for x in v.cpu()] for k, v in sums.items()}
     roofline = make_roofline(args, models, slab, per_kernel, ms_step)
     hist = 1 if "histogram" in models else 0
-    if fused:  # range init, weight table, fused fit, range->pair, pair->eps per model, stencil + 2 count kernels per model
+    if fuse_uniform:  # fused fit + stencil, range->pair, pair->eps, pending rows, 2 count kernels
+        launches_per_step = 6
+    elif fused:  # range init, weight table, fused fit, range->pair, pair->eps per model, stencil + 2 count kernels per model
         launches_per_step = 1 + hist + 1 + 1 + len(models) + 3 * len(models)
     else:
         launches_per_step = sum(5 + 2 + (1 if k == "histogram" else 0) for k in models)
@@ -391,8 +403,9 @@ def run_ours(args):
                                    f"fit + min/max/saddle for {'+'.join(models)} (bins={bins})",
                        "height": H, "width": W, "members": M, "bins": bins, "models": models,
                        "vertices_per_model": verts, "parallelism": f"row-slab x{world}",
-                       "fit": "one fused pass over the ensemble for all models" if fused else
-                              "one pass per model",
+                       "fit": ("fit and stencil fused in one kernel (cpb_fit_classify)" if fuse_uniform else
+                               "one fused pass over the ensemble for all models" if fused else
+                               "one pass per model"),
                        "l2": f"inputs ({M * H * W * 4 / 1e9:.1f} GB ensemble) larger than L2; no flush needed"},
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "parity": parity,
             "clocks": clk, "gpu_launches": launches_per_step * args.steps,
@@ -413,7 +426,10 @@ def make_roofline(args, models, slab, per_kernel, ms_step):
     kern = {}
     for (kind, what), times in per_kernel.items():
         t = statistics.mean(times)
-        if what == "fit" and kind == "fused":
+        if what == "fit+classify":  # fused uniform fit + stencil: 4M + 24 B per vertex
+            nbytes = owned_px * 4 * M + st_verts * 24
+            name = "closed_fuse_uniform_kernel"
+        elif what == "fit" and kind == "fused":
             nbytes = owned_px * (4 * M + sum(param_bytes(k, bins) for k in models))
             name = "fit_tma_multi_kernel"
         elif what == "fit":

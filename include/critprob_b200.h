@@ -178,6 +178,38 @@ int cpb_fit_multi(const float* d_ens, int64_t member_stride, cpb_field* const* f
  * CPB_ENONFINITE if any value is NaN or +-Inf. */
 int cpb_check_finite(const float* d_values, int64_t n, void* stream);
 
+/*
+ * Fused fit + closed-form stencil of a UNIFORM field, one pass over the
+ * ensemble (fields.py:137-143 + engine.py:594-629; the reference workflow
+ * classify_field(from_ensemble(stack, ModelSpec("uniform")))).  The fitted
+ * lo / hi reach the stencil through shared memory, not HBM, so the ensemble
+ * stream and the FP64 stencil overlap inside each SM.
+ *   cpb_fit_classify      fits rows [row_begin - 1, row_end] of `f` (writes those
+ *                         rows of its planes and d_range, as cpb_fit does; the full
+ *                         field for row_begin = 1, row_end = height - 1) and writes
+ *                         p_min / p_max / p_saddle for
+ *                         vertex rows [row_begin, row_end) (1 <= row_begin, row_end
+ *                         <= height - 1), except vertex rows whose stencil holds a
+ *                         degenerate pixel (lo == hi: their eps widening needs the
+ *                         GLOBAL range), which are queued in d_work;
+ *   cpb_fit_classify_finish   once f's eps is final (f->eps, or f->eps_device, e.g.
+ *                         after the cross-slab MAX all-reduce) computes the queued
+ *                         rows and ADDS the expected per-type counts of all
+ *                         [row_begin, row_end) vertices to d_counts (optional).
+ * d_work: cpb_fit_classify_work_bytes() bytes of device scratch, the same
+ * (width, row_begin, row_end) for both calls.  The one-pass kernel needs
+ * members <= 256, a 16-byte aligned ensemble with member_stride % 4 == 0 and
+ * < 2^31 pixels; other stacks are fitted by cpb_fit and stencilled in the
+ * finish pass.  Results equal cpb_fit + cpb_classify_closed bit for bit.
+ */
+int cpb_fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_end, size_t* bytes);
+int cpb_fit_classify(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
+                     int32_t accumulate, int64_t row_begin, int64_t row_end, double* d_pmin,
+                     double* d_pmax, double* d_psaddle, void* d_work, void* stream);
+int cpb_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
+                            double* d_pmax, double* d_psaddle, double* d_counts, void* d_work,
+                            void* stream);
+
 /* Synchronously read back a d_range written by cpb_fit; returns
  * CPB_ENONFINITE if any value was NaN/Inf. */
 int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* stream);

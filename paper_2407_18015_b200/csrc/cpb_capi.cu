@@ -21,6 +21,12 @@ int launch_from_scalar(const double* v, int64_t n, double half, double* lo, doub
                        cudaStream_t st);
 int launch_range_to_pair(const uint32_t* range, double* pair, cudaStream_t st);
 int launch_nonfinite(const float* v, int64_t n, uint32_t* flag, cudaStream_t st);
+size_t fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_end);
+int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
+                        bool accumulate, int64_t row_begin, int64_t row_end, double* pmin,
+                        double* pmax, double* psad, void* work, cudaStream_t st);
+int launch_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* pmin,
+                               double* pmax, double* psad, double* counts, void* work, cudaStream_t st);
 int launch_pair_to_eps(const double* pair, double* eps, cudaStream_t st);
 int launch_materialize(const cpb_field* f, double* a, double* b, double* w, cudaStream_t st);
 int launch_synth(float* ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
@@ -199,6 +205,29 @@ int cpb_read_range(const uint32_t* d_range, double* gmin, double* gmax, void* st
   if (gmin) *gmin = (double)ordered_to_float(h[0]);
   if (gmax) *gmax = (double)ordered_to_float(h[1]);
   return CPB_OK;
+}
+
+int cpb_fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_end, size_t* bytes) {
+  if (!bytes || width < 3 || row_begin > row_end) { set_error("invalid arguments"); return CPB_EINVAL; }
+  *bytes = fit_classify_work_bytes(width, row_begin, row_end);
+  return CPB_OK;
+}
+
+int cpb_fit_classify(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
+                     int32_t accumulate, int64_t row_begin, int64_t row_end, double* d_pmin,
+                     double* d_pmax, double* d_psaddle, void* d_work, void* stream) {
+  if (!d_ens || !f || !d_range || !d_work || !f->lo || !f->hi) { set_error("null argument"); return CPB_EINVAL; }
+  return launch_fit_classify(d_ens, member_stride, f, d_range, accumulate != 0, row_begin, row_end,
+                             d_pmin, d_pmax, d_psaddle, d_work, (cudaStream_t)stream);
+}
+
+int cpb_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
+                            double* d_pmax, double* d_psaddle, double* d_counts, void* d_work,
+                            void* stream) {
+  if (int rc = check_field(f, true)) return rc;
+  if (!d_work) { set_error("null workspace"); return CPB_EINVAL; }
+  return launch_fit_classify_finish(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle, d_counts, d_work,
+                                    (cudaStream_t)stream);
 }
 
 int cpb_check_finite(const float* d_values, int64_t n, void* stream) {

@@ -21,6 +21,7 @@
 #include <algorithm>
 
 #include "cpb_common.cuh"
+#include "cpb_tma.cuh"
 
 namespace cpb {
 namespace {
@@ -629,6 +630,214 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
     if (psad) psad[idx] = res[2];
   }
   if (partial) warp_partial_sums(res[0], res[1], res[2], partial);
+}
+
+// ------------------------------------------- fused fit + uniform stencil
+// One pass over the ensemble for a UNIFORM field: the fit (fields.py:137-143)
+// and the closed-form stencil (engine.py:594-629) in the same CTA, so the
+// fitted lo / hi reach the stencil through a shared-memory row ring instead of
+// HBM, and the FP64 stencil of one row overlaps the TMA stream of the next.
+//
+// Work item = (column band, segment of vertex rows).  A CTA of kFuseCols
+// threads owns kFuseCols consecutive pixel columns (kFuseOut vertex columns,
+// a halo column left, the rest right) and walks its segment's rows top to
+// bottom (one halo row above and below): per row, ONE 2-D TMA box
+// (kFuseCols pixels x M members, UTMALDG) lands in a single shared stage, each
+// thread reduces its column's members (FMNMX3.NAN / FMNMX3) into a 4-row ring
+// of (lo, hi), one barrier, the next row's TMA is issued, and vertex row r - 1
+// is stencilled from ring rows r - 2, r - 1, r.  Items come from an atomic
+// work counter (persistent CTAs, dynamic balance).
+//
+// The fitted planes are also written (they are the field's params and the
+// input of the finish pass).  A band-row whose stencil touches a degenerate
+// pixel (lo == hi: the eps widening needs the GLOBAL range, unknown until the
+// whole ensemble is read) is not computed here: it is queued in `pending`
+// and computed by closed_fuse_pending_kernel once eps is final.
+// kFuseOut: vertex columns per band = the band stride, a multiple of 4 so every
+// TMA box starts on a 16-byte boundary (threads kFuseOut + 1.. only fit halo columns)
+constexpr int kFuseCols = 128, kFuseOut = kFuseCols - 4, kFuseSeg = 128;
+constexpr int kFuseMaxMembers = 256;
+constexpr int kFuseFinishBlocks = 592;
+
+struct FuseArgs {
+  int64_t height, width;       // local field (the ensemble holds every row)
+  int64_t row_begin, row_end;  // vertex rows to stencil
+  int members;
+  int nbands, nsegs;
+  int64_t nitems;
+  float* lo;
+  float* hi;
+  uint32_t* range;
+  double* pmin;
+  double* pmax;
+  double* psad;
+  double* partial;  // (nitems * kFuseCols / 32) warp triples, or null
+  int* pending;     // [0] count, then band-rows (row * nbands + band)
+  int* work;        // work counter, zero at launch
+};
+
+__global__ void __launch_bounds__(kFuseCols) closed_fuse_uniform_kernel(
+    const __grid_constant__ CUtensorMap map, FuseArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int M = a.members, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  float* stage = reinterpret_cast<float*>(smem);                     // [M][kFuseCols]
+  float2* ring = reinterpret_cast<float2*>(stage + (size_t)M * kFuseCols);  // [4][kFuseCols]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 4 * kFuseCols);
+  __shared__ int64_t s_item;
+  if (t == 0) {
+    prefetch_tensormap(&map);
+    mbar_init(full, 1);
+    fence_mbar_init();
+  }
+  const uint64_t pol = policy_evict_first();
+  const uint32_t box_bytes = (uint32_t)M * kFuseCols * 4u;
+  uint32_t phase = 0;
+  float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
+  bool bad = false;
+  for (;;) {
+    __syncthreads();  // the previous item is done with the stage and the ring
+    if (t == 0) s_item = atomicAdd(a.work, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.nitems) break;
+    const int band = (int)(item % a.nbands);
+    const int64_t seg = item / a.nbands;
+    const int64_t c0 = (int64_t)band * kFuseOut;  // first fitted column
+    const int64_t v0 = a.row_begin + seg * kFuseSeg;
+    const int64_t v1 = min(v0 + (int64_t)kFuseSeg, a.row_end);
+    const int64_t f0 = v0 - 1;                   // fitted rows [f0, v1]
+    const int nfit = (int)(v1 - v0) + 2;
+    const int64_t c = c0 + t;
+    const bool col_ok = c < a.width;
+    // column / row ownership of the plane writes (each pixel written once)
+    const bool own_col = col_ok && ((t >= 1 && t <= kFuseOut) || c == 0 || c == a.width - 1);
+    if (t == 0) {
+      mbar_arrive_expect_tx(full, box_bytes);
+      tma_load_2d(stage, &map, (int)(f0 * a.width + c0), 0, full, pol);
+    }
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    unsigned degmask = 0;  // bit j % 4: ring row j holds a degenerate pixel
+    for (int j = 0; j < nfit; ++j) {
+      const int64_t r = f0 + j;
+      mbar_wait(full, phase);
+      phase ^= 1u;
+      // fit: this thread's column over the members (NaN-propagating min)
+      float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
+      const float* col = stage + t;
+      int m = 0;
+      for (; m + 2 <= M; m += 2) {
+        const float x0 = col[m * kFuseCols], x1 = col[(m + 1) * kFuseCols];
+        float r3;
+        asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r3) : "f"(lo), "f"(x0), "f"(x1));
+        lo = r3;
+        hi = fmaxf(hi, fmaxf(x0, x1));
+      }
+      if (m < M) {
+        const float x = col[m * kFuseCols];
+        float r2;
+        asm("min.NaN.f32 %0, %1, %2;" : "=f"(r2) : "f"(lo), "f"(x));
+        lo = r2;
+        hi = fmaxf(hi, x);
+      }
+      ring[(j & 3) * kFuseCols + t] = make_float2(lo, hi);
+      const bool live = col_ok && r < a.height;
+      if (live) {
+        bad |= ((__float_as_uint(lo) & 0x7f800000u) == 0x7f800000u) |
+               ((__float_as_uint(hi) & 0x7f800000u) == 0x7f800000u);
+        vmin = fminf(vmin, lo);
+        vmax = fmaxf(vmax, hi);
+        const bool own_row = (r >= v0 && r < v1) || (r == 0) || (r == a.height - 1 && r == v1);
+        if (own_col && own_row) {
+          a.lo[r * a.width + c] = lo;
+          a.hi[r * a.width + c] = hi;
+        }
+      }
+      const int rowdeg = __syncthreads_or(live && !(hi > lo));
+      if (t == 0 && j + 1 < nfit) {  // every thread is done with the stage
+        mbar_arrive_expect_tx(full, box_bytes);
+        tma_load_2d(stage, &map, (int)((r + 1) * a.width + c0), 0, full, pol);
+      }
+      degmask = (degmask & ~(1u << (j & 3))) | ((rowdeg ? 1u : 0u) << (j & 3));
+      if (j < 2) continue;
+      // stencil vertex row r - 1 from ring rows j - 2 (N), j - 1 (C, E, W), j (S)
+      const int64_t vr = r - 1;
+      const unsigned need = (1u << (j & 3)) | (1u << ((j - 1) & 3)) | (1u << ((j - 2) & 3));
+      if (degmask & need) {
+        if (t == 0) {
+          const int q = atomicAdd(a.pending, 1);
+          a.pending[1 + q] = (int)(vr * a.nbands + band);
+        }
+        continue;
+      }
+      if (t >= 1 && t <= kFuseOut && c <= a.width - 2) {
+        const float2 pc = ring[((j - 1) & 3) * kFuseCols + t];
+        const float2 pe = ring[((j - 1) & 3) * kFuseCols + t + 1];
+        const float2 pn = ring[((j - 2) & 3) * kFuseCols + t];
+        const float2 pw = ring[((j - 1) & 3) * kFuseCols + t - 1];
+        const float2 ps = ring[(j & 3) * kFuseCols + t];
+        const float rl[5] = {pc.x, pe.x, pn.x, pw.x, ps.x};
+        const float rh[5] = {pc.y, pe.y, pn.y, pw.y, ps.y};
+        double lo5[5], hi5[5], acc[4];
+#pragma unroll
+        for (int p = 0; p < 5; ++p) {
+          lo5[p] = (double)rl[p];
+          hi5[p] = (double)rh[p];
+        }
+        uniform_integrals_f32keys(rl, rh, lo5, hi5, acc);
+        const int64_t idx = vr * a.width + c;
+        store(a.pmin, a.pmax, a.psad, idx, acc);
+        s0 += acc[0];
+        s1 += acc[1];
+        s2 += acc[2] + acc[3];
+      }
+    }
+    if (a.partial) {  // this item's warp partials (fixed tree: deterministic)
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, d);
+      }
+      if (lane == 0) {
+        double* q = a.partial + 3 * (item * (kFuseCols / 32) + warp);
+        q[0] = s0;
+        q[1] = s1;
+        q[2] = s2;
+      }
+    }
+  }
+  merge_range(vmin, vmax, bad, a.range);
+}
+
+// The band-rows the fused kernel left for the final eps: the ordinary uniform
+// vertex code (load_bounds widens degenerate pixels by eps / 2) over the fitted
+// planes.  Block b takes pending entries b, b + grid, ... (fixed order).
+// pending[0] == -1 (the fallback when the ensemble cannot be TMA-streamed):
+// every band-row of [row_begin, row_end).
+__global__ void __launch_bounds__(kFuseCols) closed_fuse_pending_kernel(
+    FieldView f, const int* pending, int nbands, int64_t row_begin, int64_t row_end, double* pmin,
+    double* pmax, double* psad, double* partial) {
+  const int t = threadIdx.x;
+  const bool all = pending[0] < 0;
+  const int64_t count = all ? (row_end - row_begin) * nbands : pending[0];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t e = blockIdx.x; e < count; e += gridDim.x) {
+    const int64_t code = all ? row_begin * nbands + e : pending[1 + e];
+    const int64_t vr = code / nbands;
+    const int64_t c = (int64_t)(code % nbands) * kFuseOut + t;
+    if (t < 1 || t > kFuseOut || c > f.width - 2) continue;
+    const int64_t idx = vr * f.width + c;
+    const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
+    double lo[5], hi[5], acc[4];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
+    uniform_integrals(lo, hi, acc);
+    store(pmin, pmax, psad, idx, acc);
+    s0 += acc[0];
+    s1 += acc[1];
+    s2 += acc[2] + acc[3];
+  }
+  if (partial) warp_partial_sums(s0, s1, s2, partial);
 }
 
 // --------------------------------------------------------- combinatorial
@@ -1648,6 +1857,118 @@ int launch_combinatorial(const cpb_field* fld, int64_t row_begin, int64_t row_en
   combinatorial_kernel<<<(unsigned)((nvert + kCombWarps - 1) / kCombWarps), kCombWarps * 32, 0, st>>>(
       f, row_begin, nvert, cols, pmin, pmax, psad);
   CPB_CHECK_LAUNCH("combinatorial kernel");
+  return CPB_OK;
+}
+
+bool encode_tensor_map_2d_f32(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1,
+                              uint64_t stride1_bytes, uint32_t box0, uint32_t box1);
+int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range, bool accumulate,
+               cudaStream_t st);
+
+// ---- fused fit + uniform stencil (closed_fuse_uniform_kernel) -------------
+namespace {
+struct FuseLayout {
+  int nbands;
+  int64_t nsegs, nitems, max_pending;
+  size_t off_pending, off_partial, off_chunk, bytes;
+};
+FuseLayout fuse_layout(int64_t width, int64_t row_begin, int64_t row_end) {
+  FuseLayout L;
+  L.nbands = (int)((width - 2 + kFuseOut - 1) / kFuseOut);
+  const int64_t rows = std::max<int64_t>(0, row_end - row_begin);
+  L.nsegs = (rows + kFuseSeg - 1) / kFuseSeg;
+  L.nitems = L.nsegs * L.nbands;
+  L.max_pending = rows * L.nbands;
+  L.off_pending = 16;
+  L.off_partial = (L.off_pending + 4 * (size_t)(1 + L.max_pending) + 15) / 16 * 16;
+  const size_t ntrip = (size_t)L.nitems * (kFuseCols / 32) + (size_t)kFuseFinishBlocks * (kFuseCols / 32);
+  L.off_chunk = L.off_partial + ntrip * 3 * sizeof(double);
+  L.bytes = L.off_chunk + (size_t)kCountChunks * 3 * sizeof(double);
+  return L;
+}
+}  // namespace
+
+size_t fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_end) {
+  return fuse_layout(width, row_begin, row_end).bytes;
+}
+
+int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint32_t* range,
+                        bool accumulate, int64_t row_begin, int64_t row_end, double* pmin,
+                        double* pmax, double* psad, void* work, cudaStream_t st) {
+  const int64_t H = fld->height, W = fld->width, M = fld->members;
+  if (fld->kind != CPB_UNIFORM) {
+    set_error("the fused fit + stencil is for uniform fields");
+    return CPB_EINVAL;
+  }
+  if (W < 3 || row_begin < 1 || row_end > H - 1 || row_begin > row_end) {
+    set_error("fused fit + stencil: vertex rows must lie inside [1, height - 1)");
+    return CPB_EINVAL;
+  }
+  const FuseLayout L = fuse_layout(W, row_begin, row_end);
+  char* wb = static_cast<char*>(work);
+  if (M < 1 || M > kFuseMaxMembers || mstride % 4 != 0 || (reinterpret_cast<uintptr_t>(ens) & 15) ||
+      H * W >= ((int64_t)1 << 31)) {
+    // not TMA-streamable: the plain fit now, every vertex row in the finish pass
+    if (int rc = launch_fit(ens, mstride, fld, range, accumulate, st)) return rc;
+    cudaError_t e = cudaMemsetAsync(wb + L.off_pending, 0xff, 4, st);  // pending count = -1: all rows
+    if (e == cudaSuccess)  // no item partials from the one-pass kernel
+      e = cudaMemsetAsync(wb + L.off_partial, 0, (size_t)L.nitems * (kFuseCols / 32) * 3 * sizeof(double), st);
+    return e == cudaSuccess ? CPB_OK : cuda_status(e, "memset");
+  }
+  fld->bounds = CPB_BOUNDS_F32_FITTED;
+  fld->weights_mode = CPB_WEIGHTS_F64;
+  cudaError_t e = cudaMemsetAsync(wb, 0, L.off_pending + 4, st);  // work counter, pending count
+  if (e != cudaSuccess) return cuda_status(e, "memset");
+  if (!accumulate) {  // {ordered min = all ones, ordered max = 0, non-finite = 0}
+    e = cudaMemsetAsync(range, 0xff, sizeof(uint32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(range + 1, 0, 2 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return cuda_status(e, "range init");
+  }
+  CUtensorMap map;
+  if (!encode_tensor_map_2d_f32(&map, ens, (uint64_t)(H * W), (uint64_t)M, (uint64_t)mstride * 4,
+                                kFuseCols, (uint32_t)M)) {
+    set_error("cuTensorMapEncodeTiled failed");
+    return CPB_ECUDA;
+  }
+  FuseArgs a;
+  a.height = H; a.width = W; a.row_begin = row_begin; a.row_end = row_end; a.members = (int)M;
+  a.nbands = L.nbands; a.nsegs = (int)L.nsegs; a.nitems = L.nitems;
+  a.lo = static_cast<float*>(fld->lo); a.hi = static_cast<float*>(fld->hi); a.range = range;
+  a.pmin = pmin; a.pmax = pmax; a.psad = psad;
+  a.partial = reinterpret_cast<double*>(wb + L.off_partial);
+  a.pending = reinterpret_cast<int*>(wb + L.off_pending);
+  a.work = reinterpret_cast<int*>(wb);
+  const size_t smem = (size_t)M * kFuseCols * 4 + 4 * kFuseCols * sizeof(float2) + 16;
+  cudaFuncSetAttribute(closed_fuse_uniform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, closed_fuse_uniform_kernel, kFuseCols, smem);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.nitems, (int64_t)sms * std::max(per_sm, 1)));
+  if (L.nitems > 0) {
+    closed_fuse_uniform_kernel<<<(unsigned)grid, kFuseCols, smem, st>>>(map, a);
+    CPB_CHECK_LAUNCH("fused fit + uniform stencil");
+  }
+  return CPB_OK;
+}
+
+int launch_fit_classify_finish(const cpb_field* fld, int64_t row_begin, int64_t row_end, double* pmin,
+                               double* pmax, double* psad, double* counts, void* work, cudaStream_t st) {
+  const FieldView f = make_view(*fld);
+  const FuseLayout L = fuse_layout(f.width, row_begin, row_end);
+  char* wb = static_cast<char*>(work);
+  double* partial = reinterpret_cast<double*>(wb + L.off_partial);
+  closed_fuse_pending_kernel<<<kFuseFinishBlocks, kFuseCols, 0, st>>>(
+      f, reinterpret_cast<const int*>(wb + L.off_pending), L.nbands, row_begin, row_end, pmin, pmax, psad,
+      partial + 3 * (size_t)L.nitems * (kFuseCols / 32));
+  CPB_CHECK_LAUNCH("fused stencil: pending rows");
+  if (counts) {
+    double* chunk = reinterpret_cast<double*>(wb + L.off_chunk);
+    const int64_t n = L.nitems * (kFuseCols / 32) + (int64_t)kFuseFinishBlocks * (kFuseCols / 32);
+    counts_reduce_kernel<<<kCountChunks, 256, 0, st>>>(partial, n, chunk);
+    counts_finish_kernel<<<1, 256, 0, st>>>(chunk, kCountChunks, counts);
+    CPB_CHECK_LAUNCH("fused stencil: counts");
+  }
   return CPB_OK;
 }
 

@@ -262,6 +262,38 @@ CPB_D double pairwise_sum(const Get& get, int n) {
 // ---------------------------------------------------------------------------
 // parameter access for one pixel of a cpb_field
 // ---------------------------------------------------------------------------
+// Block-level merge of the per-thread range into the global words.
+CPB_D void merge_range(float vmin, float vmax, bool bad, uint32_t* range) {
+  uint32_t omin = float_to_ordered(vmin), omax = float_to_ordered(vmax);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, s));
+    omax = max(omax, __shfl_xor_sync(0xffffffffu, omax, s));
+  }
+  const unsigned anybad = __any_sync(0xffffffffu, bad);
+  __shared__ uint32_t s_min[32], s_max[32], s_bad[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s_min[warp] = omin; s_max[warp] = omax; s_bad[warp] = anybad; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    omin = lane < nw ? s_min[lane] : 0xffffffffu;
+    omax = lane < nw ? s_max[lane] : 0u;
+    uint32_t b = lane < nw ? s_bad[lane] : 0u;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      omin = min(omin, __shfl_xor_sync(0xffffffffu, omin, s));
+      omax = max(omax, __shfl_xor_sync(0xffffffffu, omax, s));
+      b |= __shfl_xor_sync(0xffffffffu, b, s);
+    }
+    if (lane == 0) {
+      atomicMin(range + 0, omin);
+      atomicMax(range + 1, omax);
+      if (b) atomicOr(range + 2, 1u);
+    }
+  }
+}
+
 struct FieldView {
   int kind, bins, members, bounds, wmode;
   int mixed;        // CPB_FLAG_MIXED: single-precision GL evaluation in the closed form

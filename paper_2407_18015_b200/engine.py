@@ -163,7 +163,13 @@ def classify_field(
     valid[1:-1, 1:-1] = True
     if output == "device":
         return ProbabilityField(planes[0], planes[1], planes[2], valid)
-    host = planes.cpu().numpy()  # one D2H; the channels are views of it (no host copies)
+    # one D2H into page-locked memory (torch's caching host allocator: a result
+    # array that is dropped returns its buffer for the next call, so repeated
+    # calls copy at DMA speed); the channels are views of it (no host copies)
+    host_t = torch.empty((3, H, W), dtype=torch.float64, pin_memory=True)
+    host_t.copy_(planes, non_blocking=True)
+    torch.cuda.current_stream(dev.device).synchronize()
+    host = host_t.numpy()
     mask = np.zeros((H, W), dtype=bool)
     mask[1:-1, 1:-1] = True
     return ProbabilityField(host[0], host[1], host[2], mask)

@@ -650,3 +650,105 @@ def test_closed_mixed_precision_within_stated_bound(golden):
     print("mixed-precision max |error|", worst)
     with pytest.raises(ValueError):
         cpb.EstimatorSpec(precision="fp16")
+
+
+# ---------------------------------------------------------------- fused fit + uniform stencil
+def _fused_uniform(vals, row_begin=None, row_end=None):
+    """cpb_fit_classify + cpb_fit_classify_finish on a (M, H, W) stack."""
+    import ctypes
+
+    from paper_2407_18015_b200 import _lib
+    from paper_2407_18015_b200.fields import DeviceField
+
+    lib = _lib.load()
+    M, H, W = vals.shape
+    rb = 1 if row_begin is None else row_begin
+    re_ = H - 1 if row_end is None else row_end
+    ens = torch.as_tensor(np.ascontiguousarray(vals), device="cuda")
+    dev = DeviceField("uniform", 5, M, H, W)
+    dev.allocate_fitted()
+    out = torch.full((3, H, W), -7.0, dtype=torch.float64, device="cuda")
+    out[:, [0, -1], :] = 0.0
+    out[:, :, [0, -1]] = 0.0
+    nb = ctypes.c_size_t()
+    _lib.check(lib.cpb_fit_classify_work_bytes(W, rb, re_, ctypes.byref(nb)))
+    work = torch.empty(max(1, nb.value), dtype=torch.uint8, device="cuda")
+    s = _lib.stream_ptr()
+    rng = dev.tensors["range"].data_ptr()
+    _lib.check(lib.cpb_fit_classify(ens.data_ptr(), H * W, dev.ref(), rng, 0, rb, re_,
+                                    out[0].data_ptr(), out[1].data_ptr(), out[2].data_ptr(),
+                                    work.data_ptr(), s))
+    gmin, gmax = ctypes.c_double(), ctypes.c_double()
+    _lib.check(lib.cpb_read_range(rng, ctypes.byref(gmin), ctypes.byref(gmax), s))
+    dev.eps = lib.cpb_epsilon(gmin.value, gmax.value)
+    counts = torch.zeros(3, dtype=torch.float64, device="cuda")
+    _lib.check(lib.cpb_fit_classify_finish(dev.ref(), rb, re_, out[0].data_ptr(), out[1].data_ptr(),
+                                           out[2].data_ptr(), counts.data_ptr(), work.data_ptr(), s))
+    torch.cuda.synchronize()
+    return dev, out.cpu().numpy(), counts.cpu().numpy(), (gmin.value, gmax.value)
+
+
+@pytest.mark.parametrize("shape", [(20, 3, 3), (20, 37, 130), (7, 131, 127), (64, 259, 253), (1, 5, 129),
+                                   (256, 9, 300), (33, 140, 128)])
+def test_fused_fit_classify_uniform_bitexact(shape):
+    """One-pass fit + stencil (cpb_fit_classify) == cpb_fit + cpb_classify_closed,
+    bit for bit: planes, range, every probability; expected counts = plane sums."""
+    M, H, W = shape
+    vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=H + W)
+    if H > 4 and W > 4:
+        vals[:, H // 2, W // 3] = 0.125  # degenerate pixels: rows queued for the final eps
+        vals[:, 1, 1] = vals[0, 1, 1]
+    dev, out, counts, rng = _fused_uniform(vals)
+    field = _fit(vals, "uniform")
+    ref = cpb.classify_field(field)
+    params = field.params
+    from paper_2407_18015_b200.fields import UncertainField
+
+    got = UncertainField(cpb.ModelSpec("uniform"), _device_field=dev).params
+    for k in ("lo", "hi"):
+        assert np.array_equal(got[k], params[k]), k
+    assert rng == (float(vals.min()), float(vals.max()))
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(out[c], ref.channel(ch)), (shape, ch, np.max(np.abs(out[c] - ref.channel(ch))))
+        assert abs(counts[c] - ref.channel(ch).sum()) <= 1e-9 * max(1.0, abs(counts[c]))
+    oref = orc.classify(orc.fit(vals, "uniform"), "uniform")
+    assert max(np.max(np.abs(out[c] - oref[ch])) for c, ch in enumerate(("min", "max", "saddle"))) <= CLOSED_TOL
+
+
+def test_fused_fit_classify_partial_rows_and_nonfinite():
+    M, H, W = 12, 50, 140
+    vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=1)
+    dev, out, counts, _ = _fused_uniform(vals, 5, 31)
+    ref = cpb.classify_field(_fit(vals, "uniform"))
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(out[c][5:31], ref.channel(ch)[5:31])
+        assert np.all(out[c][1:5, 1:-1] == -7.0) and np.all(out[c][31:-1, 1:-1] == -7.0)
+    bad = vals.copy()
+    bad[3, 20, 20] = np.nan
+    import ctypes
+
+    from paper_2407_18015_b200 import _lib
+
+    dev, out, counts, rng = None, None, None, None
+    with pytest.raises(ValueError):
+        _fused_uniform(bad)
+
+
+def test_fused_uniform_slab_path_matches_classify_field():
+    """distributed.fit_classify_uniform (the bench's uniform step) at G = 1."""
+    from paper_2407_18015_b200 import distributed as D
+
+    M, H, W = 16, 45, 263
+    vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=2)
+    vals[:, 10, 10] = 0.5
+    slab = D.slab_rows(H, 0, 1)
+    dev = torch.device("cuda")
+    f = D.SlabField(cpb.ModelSpec("uniform"), slab, W, M, dev)
+    out = torch.zeros((3, H, W), dtype=torch.float64, device=dev)
+    total, _ = D.fit_classify_uniform(f, torch.as_tensor(vals, device=dev), slab, out)
+    ref = cpb.classify_field(_fit(vals, "uniform"))
+    o = out.cpu().numpy()
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(o[c], ref.channel(ch)), ch
+    assert np.allclose(total.cpu().numpy(), [ref.channel(ch).sum() for ch in ("min", "max", "saddle")],
+                       rtol=1e-12)
