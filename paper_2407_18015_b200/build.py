@@ -58,7 +58,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         objs.append(obj)
         if not force and not _stale(obj, [src, __file__] + headers):
             continue
-        cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", src, "-o", obj]
+        # CPB_NVCC_EXTRA: extra -D flags for developer A/B builds (tools/build_variant.sh)
+        dev = os.environ.get("CPB_NVCC_EXTRA", "").split()
+        cmd = [nvcc(), *ARCH, *COMMON, *extra, *dev, "-c", src, "-o", obj]
         res = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(res.stderr)
         if res.returncode != 0:

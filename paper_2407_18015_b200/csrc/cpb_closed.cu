@@ -639,11 +639,14 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
 // HBM, and the FP64 stencil of one row overlaps the TMA stream of the next.
 //
 // Work item = (column band, segment of vertex rows).  A CTA of kFuseCols
-// threads owns kFuseCols consecutive pixel columns (kFuseOut vertex columns,
-// a halo column left, the rest right) and walks its segment's rows top to
-// bottom (one halo row above and below): per row, ONE 2-D TMA box
-// (kFuseCols pixels x M members, UTMALDG) lands in a single shared stage, each
-// thread reduces its column's members (FMNMX3.NAN / FMNMX3) into a 4-row ring
+// threads owns the kFuseCols columns [c0, c0 + kFuseCols), c0 a multiple of
+// kFuseCols, and walks its segment's rows top to bottom (one halo row above
+// and below): per row, ONE 2-D TMA box (kFuseBox = kFuseCols + 8 pixels x M
+// members, UTMALDG) starting 4 pixels left of the band -- so the band's own
+// 512 bytes per member row are 128-byte aligned and the two halo columns
+// come from the 16-byte edges the neighbouring bands also read -- lands in a
+// single shared stage; each thread reduces its column's members (FMNMX3.NAN /
+// FMNMX3; threads 0 and 1 also the left / right halo column) into a 4-row ring
 // of (lo, hi), one barrier, the next row's TMA is issued, and vertex row r - 1
 // is stencilled from ring rows r - 2, r - 1, r.  Items come from an atomic
 // work counter (persistent CTAs, dynamic balance).
@@ -653,9 +656,17 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
 // pixel (lo == hi: the eps widening needs the GLOBAL range, unknown until the
 // whole ensemble is read) is not computed here: it is queued in `pending`
 // and computed by closed_fuse_pending_kernel once eps is final.
-// kFuseOut: vertex columns per band = the band stride, a multiple of 4 so every
-// TMA box starts on a 16-byte boundary (threads kFuseOut + 1.. only fit halo columns)
-constexpr int kFuseCols = 128, kFuseOut = kFuseCols - 4, kFuseSeg = 128;
+#ifndef CPB_FUSE_SEG
+#define CPB_FUSE_SEG 128
+#endif
+#ifndef CPB_FUSE_MINB
+#define CPB_FUSE_MINB 4
+#endif
+#ifndef CPB_FUSE_EVICT_FIRST  // evict_normal: the halo rows / columns another item re-reads hit L2
+#define CPB_FUSE_EVICT_FIRST 0
+#endif
+constexpr int kFuseCols = 128, kFuseBox = kFuseCols + 8, kFuseRing = kFuseCols + 2;
+constexpr int kFuseSeg = CPB_FUSE_SEG;
 constexpr int kFuseMaxMembers = 256;
 constexpr int kFuseFinishBlocks = 592;
 
@@ -676,21 +687,46 @@ struct FuseArgs {
   int* work;        // work counter, zero at launch
 };
 
-__global__ void __launch_bounds__(kFuseCols) closed_fuse_uniform_kernel(
+CPB_D void fuse_fit_column(const float* col, int M, float& lo, float& hi) {
+  lo = __int_as_float(0x7f800000);
+  hi = -__int_as_float(0x7f800000);
+  int m = 0;
+  for (; m + 2 <= M; m += 2) {
+    const float x0 = col[m * kFuseBox], x1 = col[(m + 1) * kFuseBox];
+    float r3;
+    asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r3) : "f"(lo), "f"(x0), "f"(x1));
+    lo = r3;
+    hi = fmaxf(hi, fmaxf(x0, x1));
+  }
+  if (m < M) {
+    const float x = col[m * kFuseBox];
+    float r2;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r2) : "f"(lo), "f"(x));
+    lo = r2;
+    hi = fmaxf(hi, x);
+  }
+}
+
+__global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_kernel(
     const __grid_constant__ CUtensorMap map, FuseArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int M = a.members, t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  float* stage = reinterpret_cast<float*>(smem);                     // [M][kFuseCols]
-  float2* ring = reinterpret_cast<float2*>(stage + (size_t)M * kFuseCols);  // [4][kFuseCols]
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 4 * kFuseCols);
+  float* stage = reinterpret_cast<float*>(smem);                            // [M][kFuseBox]
+  float2* ring = reinterpret_cast<float2*>(stage + (size_t)M * kFuseBox);  // [4][kFuseRing]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + 4 * kFuseRing);
   __shared__ int64_t s_item;
   if (t == 0) {
     prefetch_tensormap(&map);
     mbar_init(full, 1);
     fence_mbar_init();
   }
+#if CPB_FUSE_EVICT_FIRST
   const uint64_t pol = policy_evict_first();
-  const uint32_t box_bytes = (uint32_t)M * kFuseCols * 4u;
+#else
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+#endif
+  const uint32_t box_bytes = (uint32_t)M * kFuseBox * 4u;
   uint32_t phase = 0;
   float vmin = __int_as_float(0x7f800000), vmax = -__int_as_float(0x7f800000);
   bool bad = false;
@@ -702,18 +738,19 @@ __global__ void __launch_bounds__(kFuseCols) closed_fuse_uniform_kernel(
     if (item >= a.nitems) break;
     const int band = (int)(item % a.nbands);
     const int64_t seg = item / a.nbands;
-    const int64_t c0 = (int64_t)band * kFuseOut;  // first fitted column
+    const int64_t c0 = (int64_t)band * kFuseCols;
     const int64_t v0 = a.row_begin + seg * kFuseSeg;
     const int64_t v1 = min(v0 + (int64_t)kFuseSeg, a.row_end);
-    const int64_t f0 = v0 - 1;                   // fitted rows [f0, v1]
+    const int64_t f0 = v0 - 1;  // fitted rows [f0, v1]
     const int nfit = (int)(v1 - v0) + 2;
     const int64_t c = c0 + t;
     const bool col_ok = c < a.width;
-    // column / row ownership of the plane writes (each pixel written once)
-    const bool own_col = col_ok && ((t >= 1 && t <= kFuseOut) || c == 0 || c == a.width - 1);
+    // halo column of threads 0 / 1: c0 - 1 (box column 3) / c0 + kFuseCols (box column kFuseCols + 4)
+    const int hbox = t == 0 ? 3 : kFuseCols + 4;
+    const int hring = t == 0 ? 0 : kFuseRing - 1;
     if (t == 0) {
       mbar_arrive_expect_tx(full, box_bytes);
-      tma_load_2d(stage, &map, (int)(f0 * a.width + c0), 0, full, pol);
+      tma_load_2d(stage, &map, (int)(f0 * a.width + c0 - 4), 0, full, pol);
     }
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     unsigned degmask = 0;  // bit j % 4: ring row j holds a degenerate pixel
@@ -721,25 +758,16 @@ __global__ void __launch_bounds__(kFuseCols) closed_fuse_uniform_kernel(
       const int64_t r = f0 + j;
       mbar_wait(full, phase);
       phase ^= 1u;
-      // fit: this thread's column over the members (NaN-propagating min)
-      float lo = __int_as_float(0x7f800000), hi = -__int_as_float(0x7f800000);
-      const float* col = stage + t;
-      int m = 0;
-      for (; m + 2 <= M; m += 2) {
-        const float x0 = col[m * kFuseCols], x1 = col[(m + 1) * kFuseCols];
-        float r3;
-        asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r3) : "f"(lo), "f"(x0), "f"(x1));
-        lo = r3;
-        hi = fmaxf(hi, fmaxf(x0, x1));
+      float lo, hi;
+      fuse_fit_column(stage + 4 + t, M, lo, hi);
+      float2* rrow = ring + (j & 3) * kFuseRing;
+      rrow[1 + t] = make_float2(lo, hi);
+      if (t < 2) {  // the band's halo columns (never degenerate-checked: a halo pixel
+                    // of this band is an own pixel of the next, which checks it)
+        float hl, hh;
+        fuse_fit_column(stage + hbox, M, hl, hh);
+        rrow[hring] = make_float2(hl, hh);
       }
-      if (m < M) {
-        const float x = col[m * kFuseCols];
-        float r2;
-        asm("min.NaN.f32 %0, %1, %2;" : "=f"(r2) : "f"(lo), "f"(x));
-        lo = r2;
-        hi = fmaxf(hi, x);
-      }
-      ring[(j & 3) * kFuseCols + t] = make_float2(lo, hi);
       const bool live = col_ok && r < a.height;
       if (live) {
         bad |= ((__float_as_uint(lo) & 0x7f800000u) == 0x7f800000u) |
@@ -747,7 +775,7 @@ __global__ void __launch_bounds__(kFuseCols) closed_fuse_uniform_kernel(
         vmin = fminf(vmin, lo);
         vmax = fmaxf(vmax, hi);
         const bool own_row = (r >= v0 && r < v1) || (r == 0) || (r == a.height - 1 && r == v1);
-        if (own_col && own_row) {
+        if (own_row) {
           a.lo[r * a.width + c] = lo;
           a.hi[r * a.width + c] = hi;
         }
@@ -755,26 +783,30 @@ __global__ void __launch_bounds__(kFuseCols) closed_fuse_uniform_kernel(
       const int rowdeg = __syncthreads_or(live && !(hi > lo));
       if (t == 0 && j + 1 < nfit) {  // every thread is done with the stage
         mbar_arrive_expect_tx(full, box_bytes);
-        tma_load_2d(stage, &map, (int)((r + 1) * a.width + c0), 0, full, pol);
+        tma_load_2d(stage, &map, (int)((r + 1) * a.width + c0 - 4), 0, full, pol);
       }
       degmask = (degmask & ~(1u << (j & 3))) | ((rowdeg ? 1u : 0u) << (j & 3));
       if (j < 2) continue;
       // stencil vertex row r - 1 from ring rows j - 2 (N), j - 1 (C, E, W), j (S)
       const int64_t vr = r - 1;
+      // a degenerate halo pixel is caught by the neighbouring band's own check of
+      // that row, but this band's stencil reads it too: the left / right halo
+      // columns are tested here as well
       const unsigned need = (1u << (j & 3)) | (1u << ((j - 1) & 3)) | (1u << ((j - 2) & 3));
-      if (degmask & need) {
+      const float2 hl = ring[((j - 1) & 3) * kFuseRing], hr = ring[((j - 1) & 3) * kFuseRing + kFuseRing - 1];
+      const bool halo_deg = (c0 > 0 && !(hl.y > hl.x)) || (c0 + kFuseCols < a.width && !(hr.y > hr.x));
+      if ((degmask & need) || halo_deg) {
         if (t == 0) {
           const int q = atomicAdd(a.pending, 1);
           a.pending[1 + q] = (int)(vr * a.nbands + band);
         }
         continue;
       }
-      if (t >= 1 && t <= kFuseOut && c <= a.width - 2) {
-        const float2 pc = ring[((j - 1) & 3) * kFuseCols + t];
-        const float2 pe = ring[((j - 1) & 3) * kFuseCols + t + 1];
-        const float2 pn = ring[((j - 2) & 3) * kFuseCols + t];
-        const float2 pw = ring[((j - 1) & 3) * kFuseCols + t - 1];
-        const float2 ps = ring[(j & 3) * kFuseCols + t];
+      if (c >= 1 && c <= a.width - 2) {
+        const float2* rn = ring + ((j - 2) & 3) * kFuseRing + 1 + t;
+        const float2* rc = ring + ((j - 1) & 3) * kFuseRing + 1 + t;
+        const float2* rs = ring + (j & 3) * kFuseRing + 1 + t;
+        const float2 pc = rc[0], pe = rc[1], pw = rc[-1], pn = rn[0], ps = rs[0];
         const float rl[5] = {pc.x, pe.x, pn.x, pw.x, ps.x};
         const float rh[5] = {pc.y, pe.y, pn.y, pw.y, ps.y};
         double lo5[5], hi5[5], acc[4];
@@ -824,8 +856,8 @@ __global__ void __launch_bounds__(kFuseCols) closed_fuse_pending_kernel(
   for (int64_t e = blockIdx.x; e < count; e += gridDim.x) {
     const int64_t code = all ? row_begin * nbands + e : pending[1 + e];
     const int64_t vr = code / nbands;
-    const int64_t c = (int64_t)(code % nbands) * kFuseOut + t;
-    if (t < 1 || t > kFuseOut || c > f.width - 2) continue;
+    const int64_t c = (int64_t)(code % nbands) * kFuseCols + t;
+    if (c < 1 || c > f.width - 2) continue;
     const int64_t idx = vr * f.width + c;
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
     double lo[5], hi[5], acc[4];
@@ -1874,7 +1906,7 @@ struct FuseLayout {
 };
 FuseLayout fuse_layout(int64_t width, int64_t row_begin, int64_t row_end) {
   FuseLayout L;
-  L.nbands = (int)((width - 2 + kFuseOut - 1) / kFuseOut);
+  L.nbands = (int)((width + kFuseCols - 1) / kFuseCols);
   const int64_t rows = std::max<int64_t>(0, row_end - row_begin);
   L.nsegs = (rows + kFuseSeg - 1) / kFuseSeg;
   L.nitems = L.nsegs * L.nbands;
@@ -1926,7 +1958,7 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint3
   }
   CUtensorMap map;
   if (!encode_tensor_map_2d_f32(&map, ens, (uint64_t)(H * W), (uint64_t)M, (uint64_t)mstride * 4,
-                                kFuseCols, (uint32_t)M)) {
+                                kFuseBox, (uint32_t)M)) {
     set_error("cuTensorMapEncodeTiled failed");
     return CPB_ECUDA;
   }
@@ -1938,7 +1970,7 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint3
   a.partial = reinterpret_cast<double*>(wb + L.off_partial);
   a.pending = reinterpret_cast<int*>(wb + L.off_pending);
   a.work = reinterpret_cast<int*>(wb);
-  const size_t smem = (size_t)M * kFuseCols * 4 + 4 * kFuseCols * sizeof(float2) + 16;
+  const size_t smem = (size_t)M * kFuseBox * 4 + 4 * kFuseRing * sizeof(float2) + 16;
   cudaFuncSetAttribute(closed_fuse_uniform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
