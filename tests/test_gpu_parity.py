@@ -194,6 +194,20 @@ def test_closed_form_offsets_and_degenerate(golden):
                 assert err <= CLOSED_TOL, (name, kind, bins, ch, err)
 
 
+@pytest.mark.parametrize("bins", [9, 16, 32, 64])
+def test_closed_form_many_bins(golden, bins):
+    """bins > 8 (closed_hist_otf_kernel: states derived on the fly from cumulative
+    counts): far-offset, degenerate, constant and random stacks against the oracle."""
+    fit = golden["fit"]
+    for name in ("offset", "degenerate", "constant", "wide", "rand"):
+        vals = fit[f"ens/{name}"]
+        ref = orc.classify(orc.fit(vals, "histogram", bins), "histogram")
+        prob = cpb.classify_field(_fit(vals, "histogram", bins))
+        for ch in ("min", "max", "saddle"):
+            err = np.max(np.abs(prob.channel(ch) - ref[ch]))
+            assert err <= CLOSED_TOL, (name, bins, ch, err)
+
+
 def test_channel_subset_and_validation(golden):
     vals = golden["fit"]["ens/rand"]
     field = _fit(vals, "uniform")
