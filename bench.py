@@ -82,8 +82,10 @@ def parse():
     p.add_argument("--precision", choices=("fp64", "mixed"), default="fp64",
                    help="closed form: fp64 (reference parity ~1e-15) or mixed (FP32 GL evaluation "
                         "for uniform / Epanechnikov, stated bound 1e-6)")
-    p.add_argument("--fit", choices=("fused", "separate"), default="fused",
-                   help="fused: one cpb_fit_multi pass over the ensemble for all models per step; "
+    p.add_argument("--fit", choices=("fused", "fused-stencil", "separate"), default="fused",
+                   help="fused: one cpb_fit_multi pass over the ensemble for all models per step "
+                        "(a uniform-only step fuses its stencil into the pass, cpb_fit_classify); "
+                        "fused-stencil: the pass also runs the uniform stencil (cpb_fit_multi_classify); "
                         "separate: one cpb_fit per model")
     p.add_argument("--fit-ctas", type=int, default=0,
                    help="persistent fit CTAs per SM while overlapping (0 = occupancy maximum)")
@@ -275,11 +277,18 @@ def run_ours(args):
     # previous stencils (FP64 bound) on a low-priority one
     s_fit = torch.cuda.Stream(device=device, priority=-1)
     s_cls = torch.cuda.Stream(device=device, priority=0)
-    fused = args.fit == "fused" and len(models) > 1
-    # a uniform-only step is ONE kernel: fit and stencil fused (cpb_fit_classify)
-    fuse_uniform = models == ["uniform"] and args.fit == "fused" and args.precision == "fp64"
+    fused = args.fit in ("fused", "fused-stencil") and len(models) > 1
+    # the uniform stencil runs inside the fit pass (cpb_fit_multi_classify): a
+    # uniform-only step is ONE kernel; with several models the pass also writes
+    # the other models' planes
+    # (with several models the one-pass fit is issue-bound, and folding the uniform
+    # stencil into it measured 31.0 ms vs 18.8 + 12.6 ms separately: no gain, so
+    # the default keeps them apart; --fit fused-stencil selects it)
+    fuse_uniform = ("uniform" in models and args.precision == "fp64"
+                    and ((len(models) == 1 and args.fit != "separate") or
+                         (args.fit == "fused-stencil" and bins <= 8)))
     nsets = 2 if overlap else 1
-    if fuse_uniform:
+    if fuse_uniform and len(models) == 1:
         sets = [{"uniform": D.SlabField(cpb.ModelSpec("uniform"), slab, W, M, device)}]
     elif fused:
         # all models fitted in ONE pass over the ensemble (cpb_fit_multi); two
@@ -293,17 +302,38 @@ def run_ours(args):
     consumed = [torch.cuda.Event() for _ in range(len(sets))]
     counter = [0]
     last = [0]
-    work = [None]
+    work = [None, None]
 
     def step():
         b = counter[0] % len(sets)
         counter[0] += 1
         last[0] = b
         fs = sets[b]
-        if fuse_uniform:
+        if fuse_uniform and len(models) == 1:
             timer.kind = "uniform"
             sums["uniform"], work[0] = D.fit_classify_uniform(fs["uniform"], ens, slab, outs["uniform"],
                                                               timer=timer, work=work[0])
+            return
+        if fuse_uniform:
+            timer.kind = "fused"
+            with torch.cuda.stream(s_fit if overlap else torch.cuda.current_stream()):
+                if overlap:
+                    s_fit.wait_event(consumed[b])
+                sums["uniform"], work[b] = D.fit_classify([fs[k] for k in models], ens, slab, outs["uniform"],
+                                                          timer=timer, work=work[b])
+                fitted[b].record()
+            with torch.cuda.stream(s_cls if overlap else torch.cuda.current_stream()):
+                if overlap:
+                    s_cls.wait_event(fitted[b])
+                for kind in models:
+                    if kind == "uniform":
+                        continue
+                    timer.kind = kind
+                    _, sums[kind] = D.classify_slab(fs[kind].dev, slab, est, out=outs[kind], sums=True,
+                                                    timer=timer)
+                consumed[b].record()
+            if overlap:
+                torch.cuda.current_stream().wait_stream(s_cls)
             return
         if fused:
             timer.kind = "fused"
@@ -371,8 +401,10 @@ def run_ours(args):
     expected = {k: [float(x) for x in v.cpu()] for k, v in sums.items()}
     roofline = make_roofline(args, models, slab, per_kernel, ms_step)
     hist = 1 if "histogram" in models else 0
-    if fuse_uniform:  # fused fit + stencil, range->pair, pair->eps, pending rows, 2 count kernels
+    if fuse_uniform and len(models) == 1:  # fused fit + stencil, range->pair, pair->eps, pending rows, 2 count kernels
         launches_per_step = 6
+    elif fuse_uniform:  # + weight table, eps per extra model, stencil + 2 count kernels per other model
+        launches_per_step = 6 + hist + (len(models) - 1) * 4
     elif fused:  # range init, weight table, fused fit, range->pair, pair->eps per model, stencil + 2 count kernels per model
         launches_per_step = 1 + hist + 1 + 1 + len(models) + 3 * len(models)
     else:
@@ -403,7 +435,9 @@ def run_ours(args):
                                    f"fit + min/max/saddle for {'+'.join(models)} (bins={bins})",
                        "height": H, "width": W, "members": M, "bins": bins, "models": models,
                        "vertices_per_model": verts, "parallelism": f"row-slab x{world}",
-                       "fit": ("fit and stencil fused in one kernel (cpb_fit_classify)" if fuse_uniform else
+                       "fit": ("fit and stencil fused in one kernel (cpb_fit_classify)" if fuse_uniform and len(models) == 1 else
+                               "one pass over the ensemble fits every model and stencils the uniform one "
+                               "(cpb_fit_multi_classify)" if fuse_uniform else
                                "one fused pass over the ensemble for all models" if fused else
                                "one pass per model"),
                        "l2": f"inputs ({M * H * W * 4 / 1e9:.1f} GB ensemble) larger than L2; no flush needed"},
@@ -426,7 +460,10 @@ def make_roofline(args, models, slab, per_kernel, ms_step):
     kern = {}
     for (kind, what), times in per_kernel.items():
         t = statistics.mean(times)
-        if what == "fit+classify":  # fused uniform fit + stencil: 4M + 24 B per vertex
+        if what == "fit+classify" and kind == "fused":  # every model's fit + the uniform stencil
+            nbytes = owned_px * (4 * M + sum(param_bytes(k, bins) for k in models if k != "uniform")) + st_verts * 24
+            name = f"closed_fuse_uniform_kernel<{bins if 'histogram' in models else 0}>"
+        elif what == "fit+classify":  # fused uniform fit + stencil: 4M + 24 B per vertex
             nbytes = owned_px * 4 * M + st_verts * 24
             name = "closed_fuse_uniform_kernel"
         elif what == "fit" and kind == "fused":

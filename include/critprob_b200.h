@@ -206,6 +206,16 @@ int cpb_fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_en
 int cpb_fit_classify(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
                      int32_t accumulate, int64_t row_begin, int64_t row_end, double* d_pmin,
                      double* d_pmax, double* d_psaddle, void* d_work, void* stream);
+/* cpb_fit_classify for several models of one stack (the reference workflow of
+ * fitting one EnsembleStack with every model): fields[] holds exactly one
+ * uniform field -- the one stencilled -- plus at most one histogram (<= 8 bins
+ * for the one-pass kernel), Epanechnikov and Gaussian field, all fitted in the
+ * same pass over the ensemble with the planes cpb_fit_multi writes.  Finish
+ * with cpb_fit_classify_finish on the uniform field. */
+int cpb_fit_multi_classify(const float* d_ens, int64_t member_stride, cpb_field* const* fields,
+                           int32_t n_fields, uint32_t* d_range, int32_t accumulate, int64_t row_begin,
+                           int64_t row_end, double* d_pmin, double* d_pmax, double* d_psaddle,
+                           void* d_work, void* stream);
 int cpb_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
                             double* d_pmax, double* d_psaddle, double* d_counts, void* d_work,
                             void* stream);

@@ -61,6 +61,8 @@ _SIGNATURES = {
     "cpb_fit_classify_work_bytes": (c_i32, [c_i64, c_i64, c_i64, ctypes.POINTER(ctypes.c_size_t)]),
     "cpb_fit_classify": (c_i32, [c_vp, c_i64, ctypes.POINTER(CpbField), c_vp, c_i32, c_i64, c_i64, c_vp, c_vp,
                                  c_vp, c_vp, c_vp]),
+    "cpb_fit_multi_classify": (c_i32, [c_vp, c_i64, ctypes.POINTER(ctypes.POINTER(CpbField)), c_i32, c_vp,
+                                       c_i32, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "cpb_fit_classify_finish": (c_i32, [ctypes.POINTER(CpbField), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                                         c_vp, c_vp]),
     "cpb_read_range": (c_i32, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl), c_vp]),

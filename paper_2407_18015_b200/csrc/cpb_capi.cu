@@ -22,9 +22,9 @@ int launch_from_scalar(const double* v, int64_t n, double half, double* lo, doub
 int launch_range_to_pair(const uint32_t* range, double* pair, cudaStream_t st);
 int launch_nonfinite(const float* v, int64_t n, uint32_t* flag, cudaStream_t st);
 size_t fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_end);
-int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
-                        bool accumulate, int64_t row_begin, int64_t row_end, double* pmin,
-                        double* pmax, double* psad, void* work, cudaStream_t st);
+int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* const* fields, int n,
+                        uint32_t* range, bool accumulate, int64_t row_begin, int64_t row_end,
+                        double* pmin, double* pmax, double* psad, void* work, cudaStream_t st);
 int launch_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* pmin,
                                double* pmax, double* psad, double* counts, void* work, cudaStream_t st);
 int launch_pair_to_eps(const double* pair, double* eps, cudaStream_t st);
@@ -217,8 +217,19 @@ int cpb_fit_classify(const float* d_ens, int64_t member_stride, cpb_field* f, ui
                      int32_t accumulate, int64_t row_begin, int64_t row_end, double* d_pmin,
                      double* d_pmax, double* d_psaddle, void* d_work, void* stream) {
   if (!d_ens || !f || !d_range || !d_work || !f->lo || !f->hi) { set_error("null argument"); return CPB_EINVAL; }
-  return launch_fit_classify(d_ens, member_stride, f, d_range, accumulate != 0, row_begin, row_end,
+  return launch_fit_classify(d_ens, member_stride, &f, 1, d_range, accumulate != 0, row_begin, row_end,
                              d_pmin, d_pmax, d_psaddle, d_work, (cudaStream_t)stream);
+}
+
+int cpb_fit_multi_classify(const float* d_ens, int64_t member_stride, cpb_field* const* fields,
+                           int32_t n_fields, uint32_t* d_range, int32_t accumulate, int64_t row_begin,
+                           int64_t row_end, double* d_pmin, double* d_pmax, double* d_psaddle,
+                           void* d_work, void* stream) {
+  if (!d_ens || !fields || !d_range || !d_work) { set_error("null argument"); return CPB_EINVAL; }
+  for (int i = 0; i < n_fields; ++i)
+    if (!fields[i]) { set_error("null field"); return CPB_EINVAL; }
+  return launch_fit_classify(d_ens, member_stride, fields, n_fields, d_range, accumulate != 0, row_begin,
+                             row_end, d_pmin, d_pmax, d_psaddle, d_work, (cudaStream_t)stream);
 }
 
 int cpb_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,

@@ -22,6 +22,7 @@
 
 #include "cpb_common.cuh"
 #include "cpb_tma.cuh"
+#include "cpb_fitpix.cuh"
 
 namespace cpb {
 namespace {
@@ -685,6 +686,7 @@ struct FuseArgs {
   double* partial;  // (nitems * kFuseCols / 32) warp triples, or null
   int* pending;     // [0] count, then band-rows (row * nbands + band)
   int* work;        // work counter, zero at launch
+  MultiArgs mf;     // NT >= 0: the planes of every fitted model (multi_fit_pixel)
 };
 
 CPB_D void fuse_fit_column(const float* col, int M, float& lo, float& hi) {
@@ -707,6 +709,10 @@ CPB_D void fuse_fit_column(const float* col, int M, float& lo, float& hi) {
   }
 }
 
+// NT < 0: the uniform field alone (min / max per column); NT >= 0: every model
+// of a.mf in the same pass (multi_fit_pixel<NT>: NT histogram bins, 0 = none),
+// the uniform one stencilled.
+template <int NT>
 __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_kernel(
     const __grid_constant__ CUtensorMap map, FuseArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -758,8 +764,13 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
       const int64_t r = f0 + j;
       mbar_wait(full, phase);
       phase ^= 1u;
+      const bool live = col_ok && r < a.height;
+      const bool own_row = (r >= v0 && r < v1) || (r == 0) || (r == a.height - 1 && r == v1);
       float lo, hi;
-      fuse_fit_column(stage + 4 + t, M, lo, hi);
+      if constexpr (NT < 0)
+        fuse_fit_column(stage + 4 + t, M, lo, hi);
+      else
+        multi_fit_pixel<NT>(stage + 4 + t, kFuseBox, a.mf, r * a.width + c, live && own_row, lo, hi);
       float2* rrow = ring + (j & 3) * kFuseRing;
       rrow[1 + t] = make_float2(lo, hi);
       if (t < 2) {  // the band's halo columns (never degenerate-checked: a halo pixel
@@ -768,14 +779,12 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
         fuse_fit_column(stage + hbox, M, hl, hh);
         rrow[hring] = make_float2(hl, hh);
       }
-      const bool live = col_ok && r < a.height;
       if (live) {
         bad |= ((__float_as_uint(lo) & 0x7f800000u) == 0x7f800000u) |
                ((__float_as_uint(hi) & 0x7f800000u) == 0x7f800000u);
         vmin = fminf(vmin, lo);
         vmax = fmaxf(vmax, hi);
-        const bool own_row = (r >= v0 && r < v1) || (r == 0) || (r == a.height - 1 && r == v1);
-        if (own_row) {
+        if (NT < 0 && own_row) {
           a.lo[r * a.width + c] = lo;
           a.hi[r * a.width + c] = hi;
         }
@@ -2120,14 +2129,33 @@ size_t fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_end
   return fuse_layout(width, row_begin, row_end).bytes;
 }
 
-int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint32_t* range,
-                        bool accumulate, int64_t row_begin, int64_t row_end, double* pmin,
-                        double* pmax, double* psad, void* work, cudaStream_t st) {
-  const int64_t H = fld->height, W = fld->width, M = fld->members;
-  if (fld->kind != CPB_UNIFORM) {
-    set_error("the fused fit + stencil is for uniform fields");
+int launch_fit_multi(const float* ens, int64_t mstride, cpb_field* const* fs, int n, uint32_t* range,
+                     bool accumulate, cudaStream_t st);
+
+// fields[0..n): one uniform field (stencilled) plus at most one histogram
+// (<= 8 bins), Epanechnikov and Gaussian field, fitted in the same pass.
+int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* const* fields, int n,
+                        uint32_t* range, bool accumulate, int64_t row_begin, int64_t row_end,
+                        double* pmin, double* pmax, double* psad, void* work, cudaStream_t st) {
+  if (n < 1 || n > 4 || !fields) { set_error("1..4 fields expected"); return CPB_EINVAL; }
+  cpb_field* slot[4] = {nullptr, nullptr, nullptr, nullptr};  // uniform, histogram, epan, gaussian
+  for (int i = 0; i < n; ++i) {
+    const int k = fields[i]->kind;
+    const int q = k == CPB_UNIFORM ? 0 : k == CPB_HISTOGRAM ? 1 : k == CPB_EPANECHNIKOV ? 2 : 3;
+    if (slot[q]) { set_error("at most one field per model kind"); return CPB_EINVAL; }
+    slot[q] = fields[i];
+  }
+  cpb_field* fld = slot[0];
+  if (!fld) {
+    set_error("the fused fit + stencil needs a uniform field");
     return CPB_EINVAL;
   }
+  const int64_t H = fld->height, W = fld->width, M = fld->members;
+  for (int i = 0; i < n; ++i)
+    if (fields[i]->height != H || fields[i]->width != W || fields[i]->members != M) {
+      set_error("fused fit: every field must share height, width and members");
+      return CPB_EINVAL;
+    }
   if (W < 3 || row_begin < 1 || row_end > H - 1 || row_begin > row_end) {
     set_error("fused fit + stencil: vertex rows must lie inside [1, height - 1)");
     return CPB_EINVAL;
@@ -2135,16 +2163,19 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint3
   const FuseLayout L = fuse_layout(W, row_begin, row_end);
   char* wb = static_cast<char*>(work);
   if (M < 1 || M > kFuseMaxMembers || mstride % 4 != 0 || (reinterpret_cast<uintptr_t>(ens) & 15) ||
-      H * W >= ((int64_t)1 << 31)) {
-    // not TMA-streamable: the plain fit now, every vertex row in the finish pass
-    if (int rc = launch_fit(ens, mstride, fld, range, accumulate, st)) return rc;
+      H * W >= ((int64_t)1 << 31) || (slot[1] && slot[1]->bins > kThreshBinsPix)) {
+    // not one TMA-streamed pass: the plain fit(s) now, every vertex row in the finish pass
+    int rc = n == 1 ? launch_fit(ens, mstride, fld, range, accumulate, st)
+                    : launch_fit_multi(ens, mstride, fields, n, range, accumulate, st);
+    if (rc == 1 && n > 1)  // launch_fit_multi declines this set: one fit per model
+      for (int i = 0; i < n; ++i)
+        if ((rc = launch_fit(ens, mstride, fields[i], range, accumulate || i > 0, st))) break;
+    if (rc) return rc;
     cudaError_t e = cudaMemsetAsync(wb + L.off_pending, 0xff, 4, st);  // pending count = -1: all rows
     if (e == cudaSuccess)  // no item partials from the one-pass kernel
       e = cudaMemsetAsync(wb + L.off_partial, 0, (size_t)L.nitems * (kFuseCols / 32) * 3 * sizeof(double), st);
     return e == cudaSuccess ? CPB_OK : cuda_status(e, "memset");
   }
-  fld->bounds = CPB_BOUNDS_F32_FITTED;
-  fld->weights_mode = CPB_WEIGHTS_F64;
   cudaError_t e = cudaMemsetAsync(wb, 0, L.off_pending + 4, st);  // work counter, pending count
   if (e != cudaSuccess) return cuda_status(e, "memset");
   if (!accumulate) {  // {ordered min = all ones, ordered max = 0, non-finite = 0}
@@ -2158,7 +2189,7 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint3
     set_error("cuTensorMapEncodeTiled failed");
     return CPB_ECUDA;
   }
-  FuseArgs a;
+  FuseArgs a = {};
   a.height = H; a.width = W; a.row_begin = row_begin; a.row_end = row_end; a.members = (int)M;
   a.nbands = L.nbands; a.nsegs = (int)L.nsegs; a.nitems = L.nitems;
   a.lo = static_cast<float*>(fld->lo); a.hi = static_cast<float*>(fld->hi); a.range = range;
@@ -2166,17 +2197,63 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* fld, uint3
   a.partial = reinterpret_cast<double*>(wb + L.off_partial);
   a.pending = reinterpret_cast<int*>(wb + L.off_pending);
   a.work = reinterpret_cast<int*>(wb);
+  int nt = -1;
+  if (n > 1) {  // the other models' planes come out of the same pass
+    MultiArgs& m = a.mf;
+    m.npix = H * W;
+    m.members = (int)M;
+    m.wmode = M <= 255 ? CPB_WEIGHTS_U8 : CPB_WEIGHTS_U16;
+    m.range = range;
+    for (int i = 0; i < 2; ++i) {
+      if (slot[i]) {
+        m.lo[i] = static_cast<float*>(slot[i]->lo);
+        m.hi[i] = static_cast<float*>(slot[i]->hi);
+      }
+      if (slot[2 + i]) {
+        m.mean[i] = slot[2 + i]->mean;
+        m.spread[i] = slot[2 + i]->spread;
+        slot[2 + i]->bounds = CPB_BOUNDS_F32_FITTED;
+        slot[2 + i]->weights_mode = CPB_WEIGHTS_F64;
+      }
+    }
+    nt = 0;
+    if (slot[1]) {
+      nt = slot[1]->bins;
+      m.bins = nt;
+      m.counts = slot[1]->weights;
+      m.wstride = slot[1]->plane_stride > 0 ? slot[1]->plane_stride : H * W;
+      slot[1]->bounds = CPB_BOUNDS_F32_FITTED;
+      slot[1]->weights_mode = m.wmode;
+      weight_table_kernel<<<(unsigned)((M + 256) / 256), 256, 0, st>>>(slot[1]->weight_table, (int)M);
+      CPB_CHECK_LAUNCH("weight table");
+    }
+  }
+  fld->bounds = CPB_BOUNDS_F32_FITTED;
+  fld->weights_mode = CPB_WEIGHTS_F64;
   const size_t smem = (size_t)M * kFuseBox * 4 + 4 * kFuseRing * sizeof(float2) + 16;
-  cudaFuncSetAttribute(closed_fuse_uniform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  int dev = 0, sms = 148, per_sm = 1;
+  int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, closed_fuse_uniform_kernel, kFuseCols, smem);
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.nitems, (int64_t)sms * std::max(per_sm, 1)));
-  if (L.nitems > 0) {
-    closed_fuse_uniform_kernel<<<(unsigned)grid, kFuseCols, smem, st>>>(map, a);
-    CPB_CHECK_LAUNCH("fused fit + uniform stencil");
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFuseCols, smem);
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.nitems, (int64_t)sms * std::max(per_sm, 1)));
+    if (L.nitems > 0) kern<<<(unsigned)grid, kFuseCols, smem, st>>>(map, a);
+  };
+  switch (nt) {
+    case -1: go(closed_fuse_uniform_kernel<-1>); break;
+    case 0: go(closed_fuse_uniform_kernel<0>); break;
+    case 1: go(closed_fuse_uniform_kernel<1>); break;
+    case 2: go(closed_fuse_uniform_kernel<2>); break;
+    case 3: go(closed_fuse_uniform_kernel<3>); break;
+    case 4: go(closed_fuse_uniform_kernel<4>); break;
+    case 5: go(closed_fuse_uniform_kernel<5>); break;
+    case 6: go(closed_fuse_uniform_kernel<6>); break;
+    case 7: go(closed_fuse_uniform_kernel<7>); break;
+    default: go(closed_fuse_uniform_kernel<8>); break;
   }
+  CPB_CHECK_LAUNCH("fused fit + uniform stencil");
   return CPB_OK;
 }
 

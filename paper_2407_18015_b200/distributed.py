@@ -400,15 +400,18 @@ def classify_slab(dev, slab: Slab, estimator, channels=("min", "max", "saddle"),
     return out, total
 
 
-def fit_classify_uniform(field: SlabField, ens_slab, slab: Slab, out, group=None, timer=None, work=None):
-    """Uniform field: fused fit + closed-form stencil (cpb_fit_classify) over the
-    slab's rows that have both neighbours locally, then the global eps, the halo
-    rows, the slab's first / last rows (ordinary stencil, after the exchange) and
-    the rows left for the final eps (cpb_fit_classify_finish).  Returns the
-    SUM-all-reduced expected per-type counts (3 doubles, device).
+def fit_classify(fields, ens_slab, slab: Slab, out, group=None, timer=None, work=None):
+    """One pass over the slab's ensemble: every field of ``fields`` is fitted
+    (cpb_fit_multi_classify; one of them uniform) and the uniform one is
+    stencilled in the same kernel over the rows that have both neighbours
+    locally; then the shared global eps (MAX all-reduce), ONE packed halo
+    exchange for every field, the slab's first / last rows of the uniform
+    field (ordinary stencil, after the exchange) and the rows left for the
+    final eps (cpb_fit_classify_finish).  Returns (the SUM-all-reduced expected
+    per-type counts of the uniform field, 3 device doubles; the work buffer).
 
-    ``out``: (3, local_height, W) float64 planes; ``work``: a reusable uint8
-    device buffer of cpb_fit_classify_work_bytes (allocated if None)."""
+    ``out``: (3, local_height, W) float64 planes of the uniform field;
+    ``work``: a reusable uint8 device buffer (allocated if None)."""
     import ctypes
 
     import torch
@@ -416,9 +419,11 @@ def fit_classify_uniform(field: SlabField, ens_slab, slab: Slab, out, group=None
     from . import _lib
     from .engine import EstimatorSpec, run_rows
 
+    fields = list(fields)
+    uni = next(f for f in fields if f.model.kind == "uniform")
     lib = _lib.load()
     s = _lib.stream_ptr()
-    W = field.width
+    W = uni.width
     h0, n = slab.halo_top, slab.owned
     rb, re_ = 1, max(1, n - 1)  # vertex rows of the owned view with both neighbours local
     nb = ctypes.c_size_t()
@@ -426,18 +431,21 @@ def fit_classify_uniform(field: SlabField, ens_slab, slab: Slab, out, group=None
     if work is None or work.numel() < nb.value:
         work = torch.empty(nb.value, dtype=torch.uint8, device=ens_slab.device)
     planes = [out[c, h0:].data_ptr() for c in range(3)]
-    rng = field.dev.tensors["range"].data_ptr()
+    f0 = fields[0]
+    rng = f0.dev.tensors["range"].data_ptr()
+    views = (ctypes.POINTER(_lib.CpbField) * len(fields))(*[ctypes.pointer(f.view) for f in fields])
     if timer:
         timer("fit+classify", True)
-    _lib.check(lib.cpb_fit_classify(ens_slab.data_ptr(), n * W, ctypes.byref(field.view), rng, 0, rb, re_,
-                                    *planes, work.data_ptr(), s))
+    _lib.check(lib.cpb_fit_multi_classify(ens_slab.data_ptr(), n * W, views, len(fields), rng, 0, rb, re_,
+                                          *planes, work.data_ptr(), s))
     if timer:
         timer("fit+classify", False)
-    st = field.dev.struct
-    st.bounds, st.weights_mode, st.plane_stride = field.view.bounds, field.view.weights_mode, 0
-    field.view.eps_device = field.eps_t.data_ptr()
-    _lib.check(lib.cpb_range_to_pair(rng, field.pair.data_ptr(), s))
-    finish_slab_fields([field], group)  # MAX all-reduce -> eps (device), packed halo exchange
+    for f in fields:
+        st = f.dev.struct
+        st.bounds, st.weights_mode, st.plane_stride = f.view.bounds, f.view.weights_mode, 0
+    uni.view.eps_device = uni.eps_t.data_ptr()
+    _lib.check(lib.cpb_range_to_pair(rng, f0.pair.data_ptr(), s))
+    finish_slab_fields(fields, group)  # MAX all-reduce -> eps (device), one packed halo exchange
     total = torch.zeros(3, dtype=torch.float64, device=ens_slab.device)
     est = EstimatorSpec()
     chans = {"min": out[0], "max": out[1], "saddle": out[2]}
@@ -445,11 +453,16 @@ def fit_classify_uniform(field: SlabField, ens_slab, slab: Slab, out, group=None
     a, b = slab.stencil_rows()
     edge_rows = sorted({r for r in (h0, h0 + n - 1) if a <= r < b and not (h0 + rb <= r < h0 + re_)})
     for r in edge_rows:
-        run_rows(field.dev, est, CH3, r, r + 1, chans, type_sums=total)
-    _lib.check(lib.cpb_fit_classify_finish(ctypes.byref(field.view), rb, re_, *planes, total.data_ptr(),
+        run_rows(uni.dev, est, CH3, r, r + 1, chans, type_sums=total)
+    _lib.check(lib.cpb_fit_classify_finish(ctypes.byref(uni.view), rb, re_, *planes, total.data_ptr(),
                                            work.data_ptr(), s))
     allreduce_sums(total, group)
     return total, work
+
+
+def fit_classify_uniform(field: SlabField, ens_slab, slab: Slab, out, group=None, timer=None, work=None):
+    """fit_classify for a uniform field alone."""
+    return fit_classify([field], ens_slab, slab, out, group, timer, work)
 
 
 CH3 = ("min", "max", "saddle")

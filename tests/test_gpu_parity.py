@@ -766,3 +766,34 @@ def test_fused_uniform_slab_path_matches_classify_field():
         assert np.array_equal(o[c], ref.channel(ch)), ch
     assert np.allclose(total.cpu().numpy(), [ref.channel(ch).sum() for ch in ("min", "max", "saddle")],
                        rtol=1e-12)
+
+
+def test_fused_multi_fit_classify_matches_separate():
+    """cpb_fit_multi_classify (distributed.fit_classify): one pass fits uniform,
+    Epanechnikov and histogram fields and stencils the uniform one -- planes
+    bit-identical to separate fits, uniform probabilities to classify_field."""
+    from paper_2407_18015_b200 import distributed as D
+
+    dev = torch.device("cuda")
+    for (M, H, W), bins in (((16, 45, 263), 5), ((40, 131, 256), 8), ((12, 30, 200), 3)):
+        vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=H)
+        vals[:, 10, 10] = 0.5
+        slab = D.slab_rows(H, 0, 1)
+        models = [cpb.ModelSpec("histogram", bins=bins), cpb.ModelSpec("uniform"), cpb.ModelSpec("epanechnikov")]
+        fields = [D.SlabField(m, slab, W, M, dev) for m in models]
+        out = torch.zeros((3, H, W), dtype=torch.float64, device=dev)
+        total, _ = D.fit_classify(fields, torch.as_tensor(vals, device=dev), slab, out)
+        stack = cpb.EnsembleStack(vals)
+        from paper_2407_18015_b200.fields import UncertainField
+
+        for m, f in zip(models, fields):
+            ref = cpb.UncertainField.from_ensemble(stack, m)
+            got = UncertainField(m, _device_field=f.dev)
+            for k, v in ref.params.items():
+                assert np.array_equal(got.params[k], v), (M, H, W, m.kind, k)
+        ref = cpb.classify_field(cpb.UncertainField.from_ensemble(stack, cpb.ModelSpec("uniform")))
+        o = out.cpu().numpy()
+        for c, ch in enumerate(("min", "max", "saddle")):
+            assert np.array_equal(o[c], ref.channel(ch)), ch
+        assert np.allclose(total.cpu().numpy(), [ref.channel(ch).sum() for ch in ("min", "max", "saddle")],
+                           rtol=1e-12)
