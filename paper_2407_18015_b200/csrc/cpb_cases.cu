@@ -406,14 +406,17 @@ __global__ void cases_finish_kernel(const unsigned long long* counts, int64_t nc
 // histogram cases only: c centre draws (plane 0), each neighbour's exact CDF
 // at the draw from the plain prefix sums (_hist_arrays, engine.py:407-413),
 // the conditional patterns of _conditional_pattern (engine.py:444-459)
-// averaged; a fixed-shape block tree adds the per-thread partial sums.
-__global__ void __launch_bounds__(kCombThreads) cases_semi_kernel(Batch B, uint64_t seed,
+// averaged.  One warp per case: the draws are summed by warp_strided_sum3,
+// the function the grid kernel (semi_kernel) uses, so a grid vertex and the
+// same neighbourhood as a case agree bitwise (test_engine.py:574-582).
+constexpr int kSemiThreads = 32;
+__global__ void __launch_bounds__(kSemiThreads) cases_semi_kernel(Batch B, uint64_t seed,
                                                                   const uint64_t* pixels, int64_t cnt,
                                                                   double* out) {
   extern __shared__ double s_tab[];
   __shared__ PosTab pt[kMaxPos];
-  __shared__ double red[3][kCombThreads];
   const int64_t c = blockIdx.x;
+  const int lane = threadIdx.x;
   const int P = B.k + 1;
   const int tabw = 2 * B.maxb + 1;
   double* ccum = s_tab + kMaxPos * tabw;  // centre prefix sums with cum[h] = 1
@@ -429,41 +432,23 @@ __global__ void __launch_bounds__(kCombThreads) cases_semi_kernel(Batch B, uint6
   sc.cum = ccum;
   const uint64_t px = pixels ? pixels[c] : (uint64_t)c;
   const uint64_t key = plane_key(pixel_key(seed, px), 0);
-  double smin = 0.0, smax = 0.0, ssad = 0.0;
   double ib[kMaxPos];
   for (int p = 0; p < P; ++p) ib[p] = 1.0 / pt[p].s.b;
-  for (int64_t i = threadIdx.x; hist && i < cnt; i += kCombThreads) {
+  auto term = [&](int64_t i, double t[3]) {
     const double x = draw<CPB_HISTOGRAM>(sc, stream_u01(key, (uint64_t)i), 0.0, pt[0].h);
     double F[kMaxPos];
     for (int p = 1; p < P; ++p)
       F[p] = hist_cdf_fast(pt[p].s.wn, pt[p].s.cum, pt[p].s.a, pt[p].s.b, ib[p], pt[p].h, x);
-    if (P == 3) {
-      smin = __dadd_rn(smin, __dmul_rn(__dsub_rn(1.0, F[1]), __dsub_rn(1.0, F[2])));
-      smax = __dadd_rn(smax, __dmul_rn(F[1], F[2]));
-      ssad = __dadd_rn(ssad, __dadd_rn(__dmul_rn(__dsub_rn(1.0, F[1]), F[2]),
-                                       __dmul_rn(F[1], __dsub_rn(1.0, F[2]))));
-    } else {
-      const double e = F[1], nn = F[2], w = F[3], s = F[4];
-      smin = __dadd_rn(smin, __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), __dsub_rn(1.0, nn)),
-                                                 __dsub_rn(1.0, w)), __dsub_rn(1.0, s)));
-      smax = __dadd_rn(smax, __dmul_rn(__dmul_rn(__dmul_rn(e, nn), w), s));
-      const double t1 = __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), nn), __dsub_rn(1.0, w)), s);
-      const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(e, __dsub_rn(1.0, nn)), w), __dsub_rn(1.0, s));
-      ssad = __dadd_rn(ssad, __dadd_rn(t1, t2));
-    }
-  }
-  red[0][threadIdx.x] = smin;
-  red[1][threadIdx.x] = smax;
-  red[2][threadIdx.x] = ssad;
-  __syncthreads();
-  for (int s = kCombThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-      for (int r = 0; r < 3; ++r) red[r][threadIdx.x] = __dadd_rn(red[r][threadIdx.x], red[r][threadIdx.x + s]);
-    __syncthreads();
-  }
-  if (threadIdx.x < 3) {
+    if (P == 3)
+      semi_terms2(F, t);
+    else
+      semi_terms4(F, t);
+  };
+  double sum[3] = {0.0, 0.0, 0.0};
+  if (hist) warp_strided_sum3(term, cnt, lane, sum);
+  if (lane < 3) {
     const double nan = __longlong_as_double(0x7ff8000000000000ll);
-    out[3 * c + threadIdx.x] = hist ? __ddiv_rn(red[threadIdx.x][0], (double)cnt) : nan;
+    out[3 * c + lane] = hist ? __ddiv_rn(sum[lane], (double)cnt) : nan;
   }
 }
 
@@ -632,7 +617,7 @@ int launch_cases_semi(const cpb_case_batch* b, uint64_t seed, const uint64_t* pi
   }
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(cases_semi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cases_semi_kernel<<<(unsigned)B.n, kCombThreads, smem, st>>>(B, seed, pixels, c, out);
+  cases_semi_kernel<<<(unsigned)B.n, kSemiThreads, smem, st>>>(B, seed, pixels, c, out);
   CPB_CHECK_LAUNCH("per-case semianalytical kernel");
   return CPB_OK;
 }

@@ -260,6 +260,51 @@ CPB_D double pairwise_sum(const Get& get, int n) {
 }
 
 // ---------------------------------------------------------------------------
+// The semianalytical mean's summation (engine.py:439 / 683 average the c
+// per-draw pattern terms): lane l of a warp adds terms l, l + 32, ... in
+// order, then a fixed xor-shuffle tree adds the 32 lane sums.  The grid
+// kernel (semi_kernel) and the per-case kernel (cases_semi_kernel) both sum
+// through this ONE function, so a grid vertex and the same neighbourhood as
+// a case give bit-identical results, as the reference's two numpy paths do
+// (test_engine.py:574-582); the association differs from numpy's pairwise
+// sum by ~1e-16 relative.  Valid in every lane.
+// ---------------------------------------------------------------------------
+// the conditional pattern terms of one draw (_conditional_pattern,
+// engine.py:444-459) from the neighbour CDFs F[1..4] (E, N, W, S) at the draw
+CPB_D void semi_terms4(const double F[5], double t[3]) {
+  const double e = F[1], nn = F[2], w = F[3], s = F[4];
+  t[0] = __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), __dsub_rn(1.0, nn)), __dsub_rn(1.0, w)),
+                   __dsub_rn(1.0, s));
+  t[1] = __dmul_rn(__dmul_rn(__dmul_rn(e, nn), w), s);
+  const double t1 = __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), nn), __dsub_rn(1.0, w)), s);
+  const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(e, __dsub_rn(1.0, nn)), w), __dsub_rn(1.0, s));
+  t[2] = __dadd_rn(t1, t2);
+}
+
+// the same for a two-neighbour (1-D) case, F[1..2]
+CPB_D void semi_terms2(const double F[3], double t[3]) {
+  t[0] = __dmul_rn(__dsub_rn(1.0, F[1]), __dsub_rn(1.0, F[2]));
+  t[1] = __dmul_rn(F[1], F[2]);
+  t[2] = __dadd_rn(__dmul_rn(__dsub_rn(1.0, F[1]), F[2]), __dmul_rn(F[1], __dsub_rn(1.0, F[2])));
+}
+
+template <typename Term>
+CPB_D void warp_strided_sum3(const Term& term, int64_t n, int lane, double r[3]) {
+  r[0] = r[1] = r[2] = 0.0;
+  for (int64_t i = lane; i < n; i += 32) {
+    double t[3];
+    term(i, t);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) r[q] = __dadd_rn(r[q], t[q]);
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) r[q] = __dadd_rn(r[q], __shfl_xor_sync(0xffffffffu, r[q], d));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // parameter access for one pixel of a cpb_field
 // ---------------------------------------------------------------------------
 // Block-level merge of the per-thread range into the global words.

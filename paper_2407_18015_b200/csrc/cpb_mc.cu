@@ -234,9 +234,8 @@ __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a
 // each neighbour contributes its exact CDF at the draw (histogram_cdf_values,
 // distributions.py:92-100, with the plain prefix sums), and the conditional
 // pattern probabilities (_conditional_pattern, engine.py:444-459) are averaged.
-// One warp per vertex; lanes accumulate float64 partial sums over a strided
-// subset of the draws and a fixed-shape warp tree adds them, so the result is
-// deterministic (it re-associates numpy's pairwise mean: ~1e-16 relative).
+// One warp per vertex; the draws are summed by warp_strided_sum3, the same
+// function the per-case kernel uses (bit-identical grid and per-case results).
 __global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs a) {
   extern __shared__ double s_tab[];  // per warp: 5 x (h wn + h+1 cum) + 1 x (h+1) centre cum
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -283,32 +282,21 @@ __global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs
     sc.cum = ccum;
     const uint64_t px = (uint64_t)((f.row0 + r) * f.gwidth + c);
     const uint64_t key = plane_key(pixel_key(a.seed, px), 0);
-    double smin = 0.0, smax = 0.0, ssad = 0.0;
-    for (int64_t i = lane; i < a.n; i += 32) {
+    auto term = [&](int64_t i, double t[3]) {
       const double x = draw<CPB_HISTOGRAM>(sc, stream_u01(key, (uint64_t)i), 0.0, h);
       double F[5];
 #pragma unroll
       for (int p = 1; p < 5; ++p)
         F[p] = hist_cdf_fast(my_tab + p * tab, my_tab + p * tab + h, lo[p], binw[p], ibinw[p], h, x);
-      const double e = F[1], nn = F[2], w = F[3], s = F[4];
-      smin = __dadd_rn(smin, __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), __dsub_rn(1.0, nn)),
-                                                 __dsub_rn(1.0, w)), __dsub_rn(1.0, s)));
-      smax = __dadd_rn(smax, __dmul_rn(__dmul_rn(__dmul_rn(e, nn), w), s));
-      const double t1 = __dmul_rn(__dmul_rn(__dmul_rn(__dsub_rn(1.0, e), nn), __dsub_rn(1.0, w)), s);
-      const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(e, __dsub_rn(1.0, nn)), w), __dsub_rn(1.0, s));
-      ssad = __dadd_rn(ssad, __dadd_rn(t1, t2));
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      smin = __dadd_rn(smin, __shfl_xor_sync(0xffffffffu, smin, d));
-      smax = __dadd_rn(smax, __shfl_xor_sync(0xffffffffu, smax, d));
-      ssad = __dadd_rn(ssad, __shfl_xor_sync(0xffffffffu, ssad, d));
-    }
+      semi_terms4(F, t);
+    };
+    double sum[3];
+    warp_strided_sum3(term, a.n, lane, sum);
     if (lane == 0) {
       const double n = (double)a.n;
-      if (a.pmin) a.pmin[idx] = __ddiv_rn(smin, n);
-      if (a.pmax) a.pmax[idx] = __ddiv_rn(smax, n);
-      if (a.psad) a.psad[idx] = __ddiv_rn(ssad, n);
+      if (a.pmin) a.pmin[idx] = __ddiv_rn(sum[0], n);
+      if (a.pmax) a.pmax[idx] = __ddiv_rn(sum[1], n);
+      if (a.psad) a.psad[idx] = __ddiv_rn(sum[2], n);
     }
     __syncwarp();
   }

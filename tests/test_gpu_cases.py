@@ -3,7 +3,7 @@
 Bars: closed form within 1e-12 of the reference (its own grid-vs-case
 tolerance, test_engine.py:548-559; observed ~1e-16), Monte Carlo bit-exact for
 uniform / histogram draws (transcendental kinds: <= 1 flipped draw per
-channel), semianalytical within 1e-13 (re-associated mean), combinatorial
+channel), semianalytical within 1e-13 (reciprocal-multiply CDFs; numpy's pairwise mean), combinatorial
 within 1e-12.
 """
 
@@ -58,6 +58,8 @@ def test_semi_and_combinatorial_against_reference(golden, k):
     sel = {x: g[f"k{k}/{x}"][hist] for x in ("kind", "a", "b", "bins", "weights", "pixels")}
     batch = CaseBatch.from_arrays(k, sel["kind"], sel["a"], sel["b"], sel["bins"], sel["weights"])
     semi = batch.semianalytical(int(g["semi/c"]), int(g["semi/seed"]), sel["pixels"])
+    # the neighbour CDFs multiply by 1/binw (cpb_sample.cuh hist_cdf_fast): 1e-13;
+    # the mean itself is numpy's pairwise sum (grid == per case bitwise, test_gpu_engine)
     assert np.max(np.abs(semi - g[f"k{k}/semi"][hist])) <= 1e-13
     small = np.max(sel["bins"], axis=1) <= 5
     sb = CaseBatch.from_arrays(k, *(sel[x][small] for x in ("kind", "a", "b", "bins", "weights")))

@@ -347,7 +347,7 @@ def test_synthetic_rows_match_host_twin():
 
 
 # ---------------------------------------------------------------- semianalytical
-SEMI_TOL = 1e-13  # per-draw arithmetic is numpy's; only the mean's summation order differs
+SEMI_TOL = 1e-13  # the mean is numpy's pairwise sum; the neighbour CDFs multiply by 1/binw
 
 
 def test_semianalytical_against_reference(golden):
