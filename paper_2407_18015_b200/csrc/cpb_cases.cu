@@ -271,6 +271,7 @@ CPB_D void load_samplers(const Batch& B, int64_t c, PosTab* pt, double* tab, int
     t.s.wn = tab + p * tabw;
     t.s.cum = tab + p * tabw + t.h;
     if (t.kind == CPB_HISTOGRAM) {
+      CPB_ASSERT(t.h >= 1 && 2 * t.h + 1 <= tabw);
       const double* w = B.w + B.woff[di];
       double* wn = tab + p * tabw;
       double* cum = wn + t.h;

@@ -772,6 +772,7 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
       else
         multi_fit_pixel<NT>(stage + 4 + t, kFuseBox, a.mf, r * a.width + c, live && own_row, lo, hi);
       float2* rrow = ring + (j & 3) * kFuseRing;
+      CPB_ASSERT(1 + t < kFuseRing && hbox < kFuseBox && hring < kFuseRing);
       rrow[1 + t] = make_float2(lo, hi);
       if (t < 2) {  // the band's halo columns (never degenerate-checked: a halo pixel
                     // of this band is an own pixel of the next, which checks it)
@@ -983,11 +984,13 @@ __global__ void __launch_bounds__(kCombWarps * 32) combinatorial_kernel(
 // cubic gives exactly 0 or 1.
 CPB_D double epan_cdf(double u) { return fma(u, fma(-0.25, u * u, 0.75), 0.5); }
 
-// epan_piece with the neighbour states given (2 bits each, from the merge
-// tags: 0 below, 1 inside, 2 above) instead of midpoint comparisons.
-template <bool FAST>
-CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, unsigned state,
-                         double s[4]) {
+// Exact-mode Epanechnikov piece (a vertex outside the fast-mode ratio, see
+// kFastRatio): 8 nodes, every node x rounded like the reference's
+// mids + halves * xi before the subtraction.  The neighbour states (2 bits
+// each, from the merge tags: 0 below, 1 inside, 2 above) replace midpoint
+// comparisons.
+CPB_D void epan_piece_exact(double a, double b, const double* m, const double* ih, unsigned state,
+                            double s[4]) {
   const double pdf0 = 0.75 * ih[C_];
   const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
   double al[5], be[5];
@@ -996,43 +999,67 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
     const unsigned c = (state >> (2 * (p - 1))) & 3u;
     const bool in = c == 1u;
     be[p] = in ? ih[p] : 0.0;
-    al[p] = in ? (FAST ? (mid - m[p]) * ih[p] : 0.0) : (c == 2u ? 1.0 : -1.0);
+    al[p] = in ? 0.0 : (c == 2u ? 1.0 : -1.0);
   }
 #pragma unroll
   for (int r = 0; r < 4; ++r) s[r] = 0.0;  // s[2] = t1 + t2, s[3] stays 0
-  if (FAST) {
-    const double uc0 = (mid - m[C_]) * ih[C_];
 #pragma unroll
-    for (int j = 0; j < GL8::n / 2; ++j) {
-      const double tau = half * GL8::x(7 - j);
-      const double wpj = GL8::w(j) * pdf0;
+  for (int j = 0; j < GL8::n; ++j) {
+    const double x = node_x(mid, half, GL8::x(j));
+    const double uc = (x - m[C_]) * ih[C_];
+    const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
+    double F[5], g[3];
 #pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const double t = side ? tau : -tau;
-        const double uc = fma(t, ih[C_], uc0);
-        const double wp = wpj * fma(-uc, uc, 1.0);
-        double F[5], g[3];
+    for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
+    integrands3(F, g);
 #pragma unroll
-        for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
-        integrands3(F, g);
-#pragma unroll
-        for (int r = 0; r < 3; ++r) s[r] = fma(wp, g[r], s[r]);
-      }
-    }
-  } else {
-#pragma unroll
-    for (int j = 0; j < GL8::n; ++j) {
-      const double x = node_x(mid, half, GL8::x(j));
-      const double uc = (x - m[C_]) * ih[C_];
-      const double wp = GL8::w(j) * (pdf0 * fma(-uc, uc, 1.0));
-      double F[5], g[3];
-#pragma unroll
-      for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(x - m[p], be[p], al[p]));
-      integrands3(F, g);
-#pragma unroll
-      for (int r = 0; r < 3; ++r) s[r] = fma(wp, g[r], s[r]);
-    }
+    for (int r = 0; r < 3; ++r) s[r] = fma(wp, g[r], s[r]);
   }
+}
+
+// Fast-mode Epanechnikov piece with nn symmetric Gauss-Legendre nodes
+// (nn = 3, 5, 6 or 8, warp-uniform; the nodes and weights are read from
+// c_glsym).  On a piece where k of the four neighbour CDFs are non-constant
+// (the others are pinned to an exact 0 or 1 by their state) the integrands
+// have degree 2 + 3k, so nn = 3, 5, 6, 8 nodes integrate them exactly for
+// k <= 1, 2, 3, 4 (the reference always uses 8, engine.py:600-601; the
+// difference is rounding).  One loop over the node pairs for every nn keeps
+// the kernel small (four unrolled variants thrashed the instruction cache).
+CPB_D void epan_piece_n(double a, double b, const double* m, const double* ih, unsigned state,
+                        int nn, double s[4]) {
+  const double pdf0 = 0.75 * ih[C_];
+  const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
+  double al[5], be[5];
+#pragma unroll
+  for (int p = 1; p < 5; ++p) {
+    const unsigned c = (state >> (2 * (p - 1))) & 3u;
+    const bool in = c == 1u;
+    be[p] = in ? ih[p] : 0.0;
+    al[p] = in ? (mid - m[p]) * ih[p] : (c == 2u ? 1.0 : -1.0);
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) s[r] = 0.0;  // s[2] = t1 + t2, s[3] stays 0
+  const double uc0 = (mid - m[C_]) * ih[C_];
+  auto node = [&](double t, double wpj) {
+    const double uc = fma(t, ih[C_], uc0);
+    const double wp = wpj * fma(-uc, uc, 1.0);
+    double F[5], g[3];
+#pragma unroll
+    for (int p = 1; p < 5; ++p) F[p] = epan_cdf(fma(t, be[p], al[p]));
+    integrands3(F, g);
+#pragma unroll
+    for (int r = 0; r < 3; ++r) s[r] = fma(wp, g[r], s[r]);
+  };
+  const int pairs = nn >> 1;
+  const int off = nn == 3 ? 2 : (nn == 5 ? 5 : (nn == 6 ? 10 : 16));
+#pragma unroll 1
+  for (int j = 0; j < pairs; ++j) {
+    const double tau = half * c_glsym[off + j];
+    const double wpj = c_glsym[off + pairs + j] * pdf0;
+    node(-tau, wpj);
+    node(tau, wpj);
+  }
+  if (nn & 1) node(0.0, c_glsym[off + 2 * pairs] * pdf0);
 }
 
 // Piece-parallel Epanechnikov stencil.  With one vertex per lane, a warp
@@ -1041,9 +1068,15 @@ CPB_D void epan_piece_st(double a, double b, const double* m, const double* ih, 
 // idle lanes.  Here each lane first builds its vertex's non-empty pieces; the
 // warp compacts all of them into one list (warp prefix sum) and then evaluates
 // it 32 pieces per round, each lane reading its piece's vertex constants from
-// shared memory.  Per-piece results land in shared memory and every vertex
-// sums its own pieces in piece order, so the result is deterministic and equal
-// to the one-vertex-per-lane kernel's summation order.
+// shared memory.  The list is sorted by piece degree class (counting sort with
+// one packed warp scan) so each round runs ONE node count on all lanes -- the
+// largest its pieces need (epan_piece_n): ~5.4 instead of 8 node evaluations
+// per piece on smooth fields.  A warp owns 32 consecutive vertices of one row
+// (row-aligned segments), so the rounds a vertex's pieces fall in, and hence
+// its rounding, do not depend on how the rows are split into launches, slabs
+// or chunks.  Per-piece results land in shared memory and every vertex sums
+// its own pieces in a fixed order (class, then piece), so the result is
+// deterministic.
 constexpr int kPPWarps = 4;
 
 // closed_pp_kernel's per-warp layout: ROWS rows of vertex constants (uniform
@@ -1110,16 +1143,17 @@ CPB_D void epan_piece_f(float a, float b, const float* m, const float* ih, unsig
 
 // Vertex constants m[5], ih[5] (+ MX: their float copies re-centred on m_C).
 template <bool MX>
-__global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
-    FieldView f, int64_t row_begin, int64_t nvert, int64_t cols, double* pmin, double* pmax,
-    double* psad, double* partial) {
+__global__ void __launch_bounds__(kPPWarps * 32, 6) closed_pp_kernel(
+    FieldView f, int64_t row_begin, int64_t row_end, int64_t cols, int64_t segs, double* pmin,
+    double* pmax, double* psad, double* partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int ROWS = MX ? 15 : 10;
   constexpr int FR = 5;  // centre ih row: sign = !fast
   PPSmem<ROWS>& S = reinterpret_cast<PPSmem<ROWS>*>(smem_raw)[warp];
-  const int64_t v = ((int64_t)blockIdx.x * kPPWarps + warp) * 32 + lane;
-  const bool live = v < nvert;
+  const int64_t g = (int64_t)blockIdx.x * kPPWarps + warp;  // row segment
+  const int64_t r = row_begin + g / segs, c = 1 + (g % segs) * 32 + lane;
+  const bool live = r < row_end && c <= cols;
   int64_t idx = 0;
   int n = 0;
   double pts[10];
@@ -1127,18 +1161,25 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   double mref = 0.0;  // MX: the centre mean, origin of the float coordinates
   bool vfast = false;
   if (live) {
-    const int64_t r = row_begin + v / cols, c = 1 + v % cols;
     idx = r * f.width + c;
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
     double lo[5], hi[5];
     bool fast = true;
     {
-      double m[5], ih[5];
+      double m[5], ih[5], sd[5];
+      // all ten loads (and eps) in flight before any use: the division's
+      // slow-path call below would otherwise serialise them per position
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
-        double hw;
-        load_epan(f, at[p], m[p], hw);
-        if (p == 0) mref = m[0];
+        m[p] = __ldg(f.mean + at[p]);
+        sd[p] = __ldg(f.spread + at[p]);
+      }
+      const double heps = __dmul_rn(0.5, field_eps(f));
+      mref = m[0];
+#pragma unroll
+      for (int p = 0; p < 5; ++p) {
+        const double ks = __dmul_rn(f.k, sd[p]);
+        const double hw = ks > heps ? ks : (heps > ks ? heps : ks);  // load_epan (fields.py:156)
         ih[p] = 1.0 / hw;
         lo[p] = m[p] - hw;  // _support_bounds, engine.py:502-505
         hi[p] = m[p] + hw;
@@ -1176,21 +1217,64 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
 #pragma unroll
     for (int i = 0; i < 9; ++i) n += pts[i + 1] > pts[i] ? 1 : 0;
   }
-  // warp exclusive prefix sum of the piece counts
-  int off = n;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, off, d);
-    if (lane >= d) off += y;
-  }
-  const int total = __shfl_sync(0xffffffffu, off, 31);
-  off -= n;
+  // Class of a piece from k, the number of neighbours inside their support on
+  // it (+1 per lo crossed, -1 per hi crossed): 0 = 8 nodes (k = 4, and every
+  // piece of an exact-mode or mixed-precision vertex), 1 = 6 (k = 3), 2 = 5
+  // (k = 2), 3 = 3 nodes (k <= 1).  Counts of classes 0..2 are packed 9-bit
+  // fields of one word (a warp holds <= 288 pieces); class 3 is the rest.
+  auto piece_class = [&](int kin) -> int {
+    if (MX || !vfast) return 0;
+    return kin >= 4 ? 0 : 4 - max(kin, 1);
+  };
+  unsigned mine = 0;  // my pieces of classes 0..2
   if (live) {
-    int q = off;
-    unsigned cnt = 0;  // crossing counts of the partition points so far (2 bits per neighbour)
+    int kin = 0;
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
       if (pts[i + 1] > pts[i]) {
+        const int cl = piece_class(kin);
+        mine += cl < 3 ? 1u << (9 * cl) : 0u;
+      }
+      if (i < 8) kin += (tg[i] & 1) ? -1 : 1;
+    }
+  }
+  // warp scans of the packed class counts and of the piece counts
+  unsigned incl = mine;
+  int incn = n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, incl, d);
+    const int yn = __shfl_up_sync(0xffffffffu, incn, d);
+    if (lane >= d) {
+      incl += y;
+      incn += yn;
+    }
+  }
+  const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+  const int total = __shfl_sync(0xffffffffu, incn, 31);
+  const int t0 = (int)(tot & 511u), t1 = (int)((tot >> 9) & 511u), t2 = (int)((tot >> 18) & 511u);
+  // first positions of my pieces: classes 0..2 packed (class bases added), class 3
+  const unsigned ex = incl - mine;
+  const unsigned start = ex + ((unsigned)t0 << 9) + ((unsigned)(t0 + t1) << 18);
+  const int ex3 = (incn - n) - (int)(ex & 511u) - (int)((ex >> 9) & 511u) - (int)((ex >> 18) & 511u);
+  const int start3 = t0 + t1 + t2 + ex3;
+  if (live) {
+    unsigned pos = start;
+    int pos3 = start3;
+    unsigned cnt = 0;
+    int kin = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      if (pts[i + 1] > pts[i]) {
+        const int cl = piece_class(kin);
+        int q;
+        if (cl < 3) {
+          q = (int)((pos >> (9 * cl)) & 511u);
+          pos += 1u << (9 * cl);
+        } else {
+          q = pos3++;
+        }
+        CPB_ASSERT(q < 9 * 32);
         if (MX && vfast) {  // float position in the first word of the slot
           reinterpret_cast<float*>(&S.pa[q])[0] = (float)(pts[i] - mref);
           reinterpret_cast<float*>(&S.pb[q])[0] = (float)(pts[i + 1] - mref);
@@ -1198,47 +1282,54 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
           S.pa[q] = pts[i];
           S.pb[q] = pts[i + 1];
         }
-        reinterpret_cast<unsigned*>(&S.r2[q])[0] = (unsigned)lane | (cnt << 8);
-        ++q;
+        reinterpret_cast<unsigned*>(&S.r2[q])[0] = (unsigned)lane | (cnt << 8) | ((unsigned)cl << 16);
       }
-      if (i < 8) cnt += 1u << (2 * (tg[i] >> 1));
+      if (i < 8) {
+        cnt += 1u << (2 * (tg[i] >> 1));
+        kin += (tg[i] & 1) ? -1 : 1;
+      }
     }
   }
   __syncwarp();
-  for (int e = lane; e < total; e += 32) {
-    const unsigned os = reinterpret_cast<const unsigned*>(&S.r2[e])[0];
+  for (int e0 = 0; e0 < total; e0 += 32) {
+    const int e = e0 + lane;
+    const bool act = e < total;
+    const unsigned os = act ? reinterpret_cast<const unsigned*>(&S.r2[e])[0] : 0u;
+    const int cl = act ? (int)((os >> 16) & 7u) : 7;
+    // the round runs the node count its most demanding piece needs (the list is
+    // sorted by class, so rounds are uniform except at class boundaries)
+    const int rc = __reduce_min_sync(0xffffffffu, cl);
+    if (!act) continue;
     const int o = (int)(os & 0xffu);
+    CPB_ASSERT(e < 9 * 32 && o < 32);
+    const unsigned st = (os >> 8) & 0xffu;
     const bool vf_ = S.vd[FR][o] > 0.0;
     const double a = S.pa[e], b = S.pb[e];
-    double s[4];
-    {
-      const unsigned st = os >> 8;
-      if (MX && vf_) {
-        const float* vf = reinterpret_cast<const float*>(&S.vd[10][0]);
-        float mf[5], ihf[5], sf[4];
-#pragma unroll
-        for (int p = 0; p < 5; ++p) {
-          mf[p] = vf[p * 32 + o];
-          ihf[p] = vf[(5 + p) * 32 + o];
-        }
-        const float fa = reinterpret_cast<const float*>(&S.pa[e])[0];
-        const float fb = reinterpret_cast<const float*>(&S.pb[e])[0];
-        epan_piece_f(fa, fb, mf, ihf, st, sf);
-        const double hf = 0.5 * (double)(fb - fa);
-        S.pa[e] = (double)sf[0] * hf;
-        S.pb[e] = (double)sf[1] * hf;
-        S.r2[e] = (double)(sf[2] + sf[3]) * hf;
-        continue;
-      }
-      double m[5], ih[5];
+    if (MX && vf_) {
+      const float* vf = reinterpret_cast<const float*>(&S.vd[10][0]);
+      float mf[5], ihf[5], sf[4];
 #pragma unroll
       for (int p = 0; p < 5; ++p) {
-        m[p] = S.vd[p][o];
-        ih[p] = p == 0 ? fabs(S.vd[5][o]) : S.vd[5 + p][o];
+        mf[p] = vf[p * 32 + o];
+        ihf[p] = vf[(5 + p) * 32 + o];
       }
-      if (vf_) epan_piece_st<true>(a, b, m, ih, st, s);
-      else epan_piece_st<false>(a, b, m, ih, st, s);
+      const float fa = reinterpret_cast<const float*>(&S.pa[e])[0];
+      const float fb = reinterpret_cast<const float*>(&S.pb[e])[0];
+      epan_piece_f(fa, fb, mf, ihf, st, sf);
+      const double hf = 0.5 * (double)(fb - fa);
+      S.pa[e] = (double)sf[0] * hf;
+      S.pb[e] = (double)sf[1] * hf;
+      S.r2[e] = (double)(sf[2] + sf[3]) * hf;
+      continue;
     }
+    double m[5], ih[5], s[4];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      m[p] = S.vd[p][o];
+      ih[p] = p == 0 ? fabs(S.vd[5][o]) : S.vd[5 + p][o];
+    }
+    if (!vf_) epan_piece_exact(a, b, m, ih, st, s);
+    else epan_piece_n(a, b, m, ih, st, rc == 0 ? 8 : (rc == 1 ? 6 : (rc == 2 ? 5 : 3)), s);
     const double half = 0.5 * (b - a);
     S.pa[e] = s[0] * half;
     S.pb[e] = s[1] * half;
@@ -1247,10 +1338,17 @@ __global__ void __launch_bounds__(kPPWarps * 32) closed_pp_kernel(
   __syncwarp();
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
   if (live) {
-    for (int q = off; q < off + n; ++q) {
-      acc[0] += S.pa[q];
-      acc[1] += S.pb[q];
-      acc[2] += S.r2[q];
+    // my pieces of class q are contiguous from their first position; sum class by class
+    const int n3 = n - (int)(mine & 511u) - (int)((mine >> 9) & 511u) - (int)((mine >> 18) & 511u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int b0 = q < 3 ? (int)((start >> (9 * q)) & 511u) : start3;
+      const int nq = q < 3 ? (int)((mine >> (9 * q)) & 511u) : n3;
+      for (int e = b0; e < b0 + nq; ++e) {
+        acc[0] += S.pa[e];
+        acc[1] += S.pb[e];
+        acc[2] += S.r2[e];
+      }
     }
     store(pmin, pmax, psad, idx, acc);
   }
@@ -1635,6 +1733,7 @@ CPB_D void hist_sweep(const double* T, int h, const int* ip, const bool* pf, dou
     t += k * K4;
     if (k == 3)
       while (t[2 * P + 1] <= x0) t += K4;
+    CPB_ASSERT(t >= T && t < T + (size_t)(h + 2) * K4);
     tp[p] = t;
     const double2 a = *reinterpret_cast<const double2*>(t);
     cc_[p] = a.x;
@@ -1701,6 +1800,7 @@ CPB_D void hist_sweep(const double* T, int h, const int* ip, const bool* pf, dou
     // pipe, were the busiest unit with all five lists re-read every piece)
     if (nextc == xn) {
       tcp += K4;
+      CPB_ASSERT(tcp < T + (size_t)(h + 2) * K4);
       pdf = tcp[1];
       nextc = tcp[2 * P + 1];
     }
@@ -1708,6 +1808,7 @@ CPB_D void hist_sweep(const double* T, int h, const int* ip, const bool* pf, dou
     for (int p = 1; p < 5; ++p) {
       if (nx[p] == xn) {
         tp[p] += K4;
+        CPB_ASSERT(tp[p] < T + (size_t)(h + 2) * K4);
         const double2 a = *reinterpret_cast<const double2*>(tp[p]);
         cc_[p] = a.x;
         ss[p] = a.y;
@@ -1767,6 +1868,7 @@ __global__ void __launch_bounds__(kTabTW * kTabTH, 2) closed_hist_tab_kernel(
   // a few ulps, so the renormalisation w / sum(w) (engine.py:538-540) is the
   // identity to within the closed form's tolerance and is skipped
   auto build = [&](int i, double lo, double hi, const double* wv, bool unit_sum) {
+    CPB_ASSERT(i >= 0 && i < P);
     const double it = unit_sum ? 1.0 : rcp(HB <= 8 ? pairwise_small<HB>(wv) : pairwise16(wv, h));
     const double width = hi - lo, binw = width * ih, ibinw = dh * rcp(width);
     const bool pfast = (fabs(lo) + fabs(hi)) * ibinw <= kFastRatio;
@@ -1913,6 +2015,7 @@ CPB_D void otf_enter(OtfList& L, int k, int h, const double* lo, const double* h
     return;
   }
   const int b = k - 1;
+  CPB_ASSERT(i >= 0 && i < P && b >= 0 && b < h);
   const int c0 = cc[b * P + i], c1 = cc[(b + 1) * P + i];
   const double cum = wt[c0], wn = wt[c1 - c0];
   const double sl = wn * fabs(ibw[i]);
@@ -2297,7 +2400,8 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
     return CPB_EINVAL;
   }
   const int64_t cols = f.width - 2, nvert = rows * cols;
-  const int64_t pp_blocks = (nvert + kPPWarps * 32 - 1) / (kPPWarps * 32);
+  const int64_t pp_segs = (cols + 31) / 32;  // closed_pp_kernel: row-aligned 32-vertex segments
+  const int64_t pp_blocks = (rows * pp_segs + kPPWarps - 1) / kPPWarps;
   // per-block partial sums of the expected counts (freed on every path)
   struct Partial {
     double* p = nullptr;
@@ -2330,7 +2434,7 @@ int launch_closed(const cpb_field* fld, int64_t row_begin, int64_t row_end, doub
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp_smem);
       kern<<<(unsigned)pp_blocks, kPPWarps * 32, pp_smem, st>>>(
-          f, row_begin, nvert, cols, pmin, pmax, psad, part.p);
+          f, row_begin, row_end, cols, pp_segs, pmin, pmax, psad, part.p);
       fused_counts = true;
       break;
     }

@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <string.h>
 
 #include "../../include/critprob_b200.h"
@@ -19,6 +20,25 @@ namespace cpb {
 // ---------------------------------------------------------------------------
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
+
+// Bounds-check build (CPB_NVCC_EXTRA=-DCPB_BOUNDS_CHECK=1, tools/build_variant.sh):
+// every CPB_ASSERT on a shared-memory / ring index traps with its location, so
+// the GPU test suite run against that build doubles as an out-of-bounds check
+// (compute-sanitizer is not available on this pool).  Compiled out otherwise.
+#if defined(CPB_BOUNDS_CHECK) && CPB_BOUNDS_CHECK
+#define CPB_ASSERT(cond)                                                                 \
+  do {                                                                                   \
+    if (!(cond)) {                                                                       \
+      printf("CPB_ASSERT failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                         \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define CPB_ASSERT(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 #define CPB_CHECK_LAUNCH(what)                                              \
   do {                                                                      \
@@ -60,57 +80,34 @@ struct GL3 {
   }
 };
 
-// Symmetric Gauss-Legendre rules by node count, as (positive node, weight)
-// pairs plus the centre weight for odd counts -- numpy leggauss(n) bits.
-// Used by the degree-adaptive Epanechnikov stencil: a piece whose integrand
-// has degree 2 + 3k (k neighbours inside their support) is integrated exactly
-// by n = 2, 3, 5, 6, 8 nodes for k = 0..4.
+// numpy leggauss(n) bits by node count, as (positive node, weight) pairs from
+// the outermost node in, plus the centre weight for odd counts; constant
+// memory like c_gl3 / c_gl8.  Offsets: n = 2 at 0, 3 at 2, 5 at 5, 6 at 10,
+// 8 at 16.
+__constant__ double c_glsym[24] = {
+    0x1.279a74590331cp-1, 0x1.0000000000000p+0,                                     // 2
+    0x1.8c97ef43f7248p-1, 0x1.1c71c71c71c73p-1, 0x1.c71c71c71c71cp-1,               // 3
+    0x1.cff6ce0533a69p-1, 0x1.13b23fd99b705p-1, 0x1.e539ec36e0393p-3,               // 5
+    0x1.ea1da25ae4158p-2, 0x1.23456789abcddp-1,
+    0x1.dd6ca4e80a01dp-1, 0x1.528a09655c95ep-1, 0x1.e8b12d03675c5p-3,               // 6
+    0x1.5edf601e2dbf5p-3, 0x1.716b7b5794c1ep-2, 0x1.df24d499545e8p-2,
+    0x1.ebab1cb0acc66p-1, 0x1.97e4ab249f41ep-1, 0x1.0d129583284b4p-1,               // 8
+    0x1.77ac94f3c7344p-3, 0x1.9ea1d04ca03aep-4, 0x1.c76fb531d2b94p-3,
+    0x1.413c50a25560ep-2, 0x1.736360b19933dp-2};
+
+// Symmetric Gauss-Legendre rule with NN nodes (device code only): x(i), w(i)
+// for the node pairs +-x(i), w0() the centre weight (odd NN).  Used by the
+// degree-adaptive Epanechnikov stencil: a piece whose integrand has degree
+// 2 + 3k (k neighbours inside their support) is integrated exactly by
+// NN = 2, 3, 5, 6, 8 nodes for k = 0..4.
 template <int NN>
-struct GLSym;
-template <>
-struct GLSym<2> {
-  static constexpr int pairs = 2 / 2;
-  CPB_HD static double x(int) { return 0x1.279a74590331cp-1; }
-  CPB_HD static double w(int) { return 0x1.0000000000000p+0; }
-  CPB_HD static double w0() { return 0.0; }
-};
-template <>
-struct GLSym<3> {
-  static constexpr int pairs = 1;
-  CPB_HD static double x(int) { return 0x1.8c97ef43f7248p-1; }
-  CPB_HD static double w(int) { return 0x1.1c71c71c71c73p-1; }
-  CPB_HD static double w0() { return 0x1.c71c71c71c71cp-1; }
-};
-template <>
-struct GLSym<5> {
-  static constexpr int pairs = 2;
-  CPB_HD static double x(int i) { return i == 0 ? 0x1.cff6ce0533a69p-1 : 0x1.13b23fd99b705p-1; }
-  CPB_HD static double w(int i) { return i == 0 ? 0x1.e539ec36e0393p-3 : 0x1.ea1da25ae4158p-2; }
-  CPB_HD static double w0() { return 0x1.23456789abcddp-1; }
-};
-template <>
-struct GLSym<6> {
-  static constexpr int pairs = 3;
-  CPB_HD static double x(int i) {
-    return i == 0 ? 0x1.dd6ca4e80a01dp-1 : (i == 1 ? 0x1.528a09655c95ep-1 : 0x1.e8b12d03675c5p-3);
-  }
-  CPB_HD static double w(int i) {
-    return i == 0 ? 0x1.5edf601e2dbf5p-3 : (i == 1 ? 0x1.716b7b5794c1ep-2 : 0x1.df24d499545e8p-2);
-  }
-  CPB_HD static double w0() { return 0.0; }
-};
-template <>
-struct GLSym<8> {
-  static constexpr int pairs = 4;
-  CPB_HD static double x(int i) {
-    return i == 0 ? 0x1.ebab1cb0acc66p-1
-                  : (i == 1 ? 0x1.97e4ab249f41ep-1 : (i == 2 ? 0x1.0d129583284b4p-1 : 0x1.77ac94f3c7344p-3));
-  }
-  CPB_HD static double w(int i) {
-    return i == 0 ? 0x1.9ea1d04ca03aep-4
-                  : (i == 1 ? 0x1.c76fb531d2b94p-3 : (i == 2 ? 0x1.413c50a25560ep-2 : 0x1.736360b19933dp-2));
-  }
-  CPB_HD static double w0() { return 0.0; }
+struct GLSym {
+  static constexpr int pairs = NN / 2;
+  static constexpr int off = NN == 2 ? 0 : NN == 3 ? 2 : NN == 5 ? 5 : NN == 6 ? 10 : 16;
+  static_assert(NN == 2 || NN == 3 || NN == 5 || NN == 6 || NN == 8, "no table");
+  CPB_D static double x(int i) { return c_glsym[off + i]; }
+  CPB_D static double w(int i) { return c_glsym[off + pairs + i]; }
+  CPB_D static double w0() { return NN % 2 ? c_glsym[off + 2 * pairs] : 0.0; }
 };
 
 struct GL8 {

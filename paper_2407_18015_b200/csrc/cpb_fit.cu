@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_kernel(const __grid_constant
   int s = 0;           // ring slot of this tile
   uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    CPB_ASSERT(s >= 0 && s < stages);
     mbar_wait(&full[s], phase);
     const float* col = buf + (size_t)s * rows * kTmaTile + tid;
     const int64_t p = t * kTmaTile + tid;
@@ -375,6 +376,7 @@ __global__ void __launch_bounds__(kTmaTile) fit_tma_multi_kernel(
   int s = 0;           // ring slot of this tile
   uint32_t phase = 0;  // mbarrier phase parity of the slot's current use
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    CPB_ASSERT(s >= 0 && s < stages);
     mbar_wait(&full[s], phase);
     const float* col = buf + (size_t)s * rows * kTmaTile + tid;
     const int64_t p = t * kTmaTile + tid;

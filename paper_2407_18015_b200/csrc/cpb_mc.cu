@@ -165,6 +165,7 @@ __global__ void __launch_bounds__(kMcWarps * 32) mc_kernel(FieldView f, McArgs a
           ty = (x0 < x1 && x0 < x3) ? 1 : ((x0 > x1 && x0 > x3) ? 2 : 0);
         }
         const unsigned m = __ballot_sync(0xffffffffu, ty != 0);
+        CPB_ASSERT(qn + __popc(m) <= 64);
         if (ty) {
           const int e = (qh + qn + __popc(m & ((1u << lane) - 1u))) & 63;
           qx[e] = x0;
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(kMcWarps * 32) semi_kernel(FieldView f, McArgs
         const double total = pairwise_sum([&](int b) { return load_weight(f, at[p], b, deg, dbin); }, h);
         double* wn = my_tab + p * tab;
         double* cum = wn + h;
+        CPB_ASSERT(p * tab + 2 * h + 1 <= 5 * tab + h + 1);
         double run = 0.0;
         cum[0] = 0.0;
         for (int b = 0; b < h; ++b) {
