@@ -493,7 +493,12 @@ def make_roofline(args, models, slab, per_kernel, ms_step):
     if os.path.exists(fpath):
         try:
             fp = json.load(open(fpath))
-            key = next((k for k in fp if k.split("<")[0] == dom["kernel"].split("<")[0]), None)
+            # FLOP counts are data- and shape-dependent: only a capture of this
+            # very workload (grid, members, bins) applies
+            wl = fp.get("_workload", {})
+            same = (wl.get("height"), wl.get("width"), wl.get("members"), wl.get("bins")) == (H, W, M, bins)
+            key = next((k for k in fp if not k.startswith("_") and
+                        k.split("<")[0] == dom["kernel"].split("<")[0]), None) if same else None
             if key:
                 r = fp[key]
                 flops = r["achieved_tflops"] * 1e12 * r["ms"] / 1e3  # per launch, from ncu
@@ -504,7 +509,7 @@ def make_roofline(args, models, slab, per_kernel, ms_step):
                            "flop_per_launch": flops,
                            "fp64_inst_frac_ncu": r["fp64_inst_frac"],
                            "fp64_pipe_active_pct_ncu": r["fp64_pipe_active_pct"],
-                           "source": f"FLOP per launch from ncu --set full ({r.get('_report', 'profiles/ncu_fp64.json')}); "
+                           "source": f"FLOP per launch from ncu --set full ({fp.get('_report', 'profiles/ncu_fp64.json')}); "
                                      "time = this run's CUDA events"}
         except Exception:
             compute = None
