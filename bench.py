@@ -798,7 +798,8 @@ def run_reference(args):
     sec = time.perf_counter() - t
     value = len(models) * nv * args.steps / sec / 1e6
     sample = (f"{vrows} vertex rows x {W - 2} columns of the config-5 ensemble ({M} members) per step, "
-              f"fit + closed form for {'+'.join(models)}; {how}")
+              f"fit + closed form for {'+'.join(models)}; {how}; eps = that of the whole ensemble "
+              f"from its analytic range (it only widens degenerate pixels; this data has none)")
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "Mvertices/s",
             "n_gpus": args.gpus, "host_cores": cores,
             "device": "host CPU only (n_gpus echoes --gpus; no GPU is used by this arm)", "steps": args.steps, "warmup": args.warmup,
