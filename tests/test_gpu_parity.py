@@ -797,3 +797,21 @@ def test_fused_multi_fit_classify_matches_separate():
             assert np.array_equal(o[c], ref.channel(ch)), ch
         assert np.allclose(total.cpu().numpy(), [ref.channel(ch).sum() for ch in ("min", "max", "saddle")],
                            rtol=1e-12)
+
+
+@pytest.mark.parametrize("members", [49, 93, 211, 255])
+def test_histogram_fitted_weights_not_renormalised(members):
+    """The table stencil uses the fitted weights count / M as they are; the
+    reference renormalises w / sum(w) first (engine.py:538-540).  For count
+    weights the sum is 1 to within an ulp (at most 2.2e-16 away over all
+    compositions of M <= 255 into 5 bins), so the skipped division moves the
+    probabilities by ~1e-16.  Pinned against the renormalising oracle at 1e-13
+    on member counts whose weight sums are furthest from 1 (5 and 7 bins: the
+    table kernels; 12 bins: states from cumulative counts)."""
+    vals = orc.ackley_ensemble(26, 22, members, noise_amp=0.3, seed=members)
+    for bins in (5, 7, 12):
+        ref = orc.classify(orc.fit(vals, "histogram", bins), "histogram")
+        prob = cpb.classify_field(_fit(vals, "histogram", bins))
+        for ch in ("min", "max", "saddle"):
+            err = np.max(np.abs(prob.channel(ch) - ref[ch]))
+            assert err <= 1e-13, (members, bins, ch, err)
