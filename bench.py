@@ -255,6 +255,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
+        # communicator-init lines on stderr (one per rank) show the N ranks and
+        # the transport (NVLink / NVLS) NCCL chose; stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=device)
         print(f"[bench] rank {rank}/{world}: NCCL process group on cuda:{local} "
               f"({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
