@@ -13,6 +13,19 @@
 
 #include "cpb_common.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
+// NVTX range around every compute entry point (header-only NVTX 3: a no-op
+// unless a tool such as Nsight Systems / Compute is attached), so a trace of
+// the reference-facing calls lines up with the kernels they launch.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define CPB_NVTX_RANGE(name) NvtxRange cpb_nvtx_range_(name)
+
 namespace cpb {
 
 int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range, bool accumulate,
@@ -139,6 +152,7 @@ int cpb_field_plane_bytes(int32_t kind, int32_t bins, int32_t members, int64_t h
 
 int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
             int32_t accumulate, void* stream) {
+  CPB_NVTX_RANGE("cpb_fit");
   int s = check_field(f, false);
   if (s) return s;
   if (f->members < 1) { set_error("ensemble needs at least one member"); return CPB_EINVAL; }
@@ -158,6 +172,7 @@ int cpb_fit(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d
 
 int cpb_fit_multi(const float* d_ens, int64_t member_stride, cpb_field* const* fields,
                   int32_t n_fields, uint32_t* d_range, int32_t accumulate, void* stream) {
+  CPB_NVTX_RANGE("cpb_fit_multi");
   if (!fields || n_fields < 1 || n_fields > 16) { set_error("1..16 fields expected"); return CPB_EINVAL; }
   for (int i = 0; i < n_fields; ++i) {
     cpb_field* f = fields[i];
@@ -216,6 +231,7 @@ int cpb_fit_classify_work_bytes(int64_t width, int64_t row_begin, int64_t row_en
 int cpb_fit_classify(const float* d_ens, int64_t member_stride, cpb_field* f, uint32_t* d_range,
                      int32_t accumulate, int64_t row_begin, int64_t row_end, double* d_pmin,
                      double* d_pmax, double* d_psaddle, void* d_work, void* stream) {
+  CPB_NVTX_RANGE("cpb_fit_classify");
   if (!d_ens || !f || !d_range || !d_work || !f->lo || !f->hi) { set_error("null argument"); return CPB_EINVAL; }
   return launch_fit_classify(d_ens, member_stride, &f, 1, d_range, accumulate != 0, row_begin, row_end,
                              d_pmin, d_pmax, d_psaddle, d_work, (cudaStream_t)stream);
@@ -225,6 +241,7 @@ int cpb_fit_multi_classify(const float* d_ens, int64_t member_stride, cpb_field*
                            int32_t n_fields, uint32_t* d_range, int32_t accumulate, int64_t row_begin,
                            int64_t row_end, double* d_pmin, double* d_pmax, double* d_psaddle,
                            void* d_work, void* stream) {
+  CPB_NVTX_RANGE("cpb_fit_multi_classify");
   if (!d_ens || !fields || !d_range || !d_work) { set_error("null argument"); return CPB_EINVAL; }
   for (int i = 0; i < n_fields; ++i)
     if (!fields[i]) { set_error("null field"); return CPB_EINVAL; }
@@ -235,6 +252,7 @@ int cpb_fit_multi_classify(const float* d_ens, int64_t member_stride, cpb_field*
 int cpb_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
                             double* d_pmax, double* d_psaddle, double* d_counts, void* d_work,
                             void* stream) {
+  CPB_NVTX_RANGE("cpb_fit_classify_finish");
   if (int rc = check_field(f, true)) return rc;
   if (!d_work) { set_error("null workspace"); return CPB_EINVAL; }
   return launch_fit_classify_finish(f, row_begin, row_end, d_pmin, d_pmax, d_psaddle, d_counts, d_work,
@@ -242,6 +260,7 @@ int cpb_fit_classify_finish(const cpb_field* f, int64_t row_begin, int64_t row_e
 }
 
 int cpb_check_finite(const float* d_values, int64_t n, void* stream) {
+  CPB_NVTX_RANGE("cpb_check_finite");
   if (n < 0 || (n > 0 && !d_values)) { set_error("invalid values"); return CPB_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* flag = nullptr;
@@ -271,6 +290,7 @@ int cpb_pair_to_eps(const double* d_pair, double* d_eps, void* stream) {
 
 int cpb_from_scalar(const double* d_values, int64_t height, int64_t width, double error_bound,
                     double eps, double* d_lo, double* d_hi, void* stream) {
+  CPB_NVTX_RANGE("cpb_from_scalar");
   if (!(error_bound >= 0.0)) { set_error("error bound must be nonnegative"); return CPB_EINVAL; }
   double half = 0.5 * error_bound;
   if (half <= 0.0) half = 0.5 * eps;  // fields.py:174-176
@@ -279,6 +299,7 @@ int cpb_from_scalar(const double* d_values, int64_t height, int64_t width, doubl
 
 int cpb_classify_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, double* d_pmin,
                         double* d_pmax, double* d_psaddle, void* stream) {
+  CPB_NVTX_RANGE("cpb_classify_closed");
   int s = check_field(f, true);
   if (s) return s;
   if (f->kind == CPB_GAUSSIAN) {
@@ -298,6 +319,7 @@ int cpb_classify_closed(const cpb_field* f, int64_t row_begin, int64_t row_end, 
 int cpb_classify_closed_counts(const cpb_field* f, int64_t row_begin, int64_t row_end,
                                double* d_pmin, double* d_pmax, double* d_psaddle, double* d_counts,
                                void* stream) {
+  CPB_NVTX_RANGE("cpb_classify_closed_counts");
   if (!d_counts) { set_error("d_counts must not be NULL"); return CPB_EINVAL; }
   int s = check_field(f, true);
   if (s) return s;
@@ -318,6 +340,7 @@ int cpb_classify_closed_counts(const cpb_field* f, int64_t row_begin, int64_t ro
 int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,
                     int64_t n_samples, int32_t rng, double* d_pmin, double* d_pmax,
                     double* d_psaddle, int64_t* d_counts, void* stream) {
+  CPB_NVTX_RANGE("cpb_classify_mc");
   int s = check_field(f, true);
   if (s) return s;
   if (rng != CPB_RNG_SPLITMIX && rng != CPB_RNG_PHILOX) { set_error("unknown rng %d", rng); return CPB_EINVAL; }
@@ -335,6 +358,7 @@ int cpb_classify_mc(const cpb_field* f, int64_t row_begin, int64_t row_end, uint
 int cpb_classify_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, uint64_t seed,
                       int64_t c, double* d_pmin, double* d_pmax, double* d_psaddle,
                       void* stream) {
+  CPB_NVTX_RANGE("cpb_classify_semi");
   int s = check_field(f, true);
   if (s) return s;
   if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
@@ -350,6 +374,7 @@ int cpb_classify_semi(const cpb_field* f, int64_t row_begin, int64_t row_end, ui
 
 int cpb_classify_combinatorial(const cpb_field* f, int64_t row_begin, int64_t row_end,
                                double* d_pmin, double* d_pmax, double* d_psaddle, void* stream) {
+  CPB_NVTX_RANGE("cpb_classify_combinatorial");
   int s = check_field(f, true);
   if (s) return s;
   if (row_begin < 1 || row_end > f->height - 1 || f->width < 3) {
@@ -365,6 +390,7 @@ int cpb_classify_combinatorial(const cpb_field* f, int64_t row_begin, int64_t ro
 
 int cpb_materialize(const cpb_field* f, double* d_a, double* d_b, double* d_weights,
                     void* stream) {
+  CPB_NVTX_RANGE("cpb_materialize");
   int s = check_field(f, true);
   if (s) return s;
   return launch_materialize(f, d_a, d_b, d_weights, (cudaStream_t)stream);
@@ -372,12 +398,14 @@ int cpb_materialize(const cpb_field* f, double* d_a, double* d_b, double* d_weig
 
 int cpb_unit_block(uint64_t seed, const uint64_t* d_pixels, int64_t npix, int32_t planes,
                    int64_t start, int64_t n, double* d_out, void* stream) {
+  CPB_NVTX_RANGE("cpb_unit_block");
   if (npix < 0 || planes < 0 || n < 0 || start < 0) { set_error("negative extent"); return CPB_EINVAL; }
   return launch_unit_block(seed, d_pixels, npix, planes, start, n, d_out, (cudaStream_t)stream);
 }
 
 int cpb_synth_ensemble(float* d_ens, int64_t members, int64_t row0, int64_t nrows, int64_t width,
                        int64_t height, double noise_amp, uint64_t seed, void* stream) {
+  CPB_NVTX_RANGE("cpb_synth_ensemble");
   if (members < 1 || nrows < 0 || width < 1 || height < 1 || row0 < 0 || row0 + nrows > height) {
     set_error("invalid synthetic ensemble extent");
     return CPB_EINVAL;
@@ -388,6 +416,7 @@ int cpb_synth_ensemble(float* d_ens, int64_t members, int64_t row0, int64_t nrow
 
 int cpb_heatmap(const double* d_p, const uint8_t* d_valid, int64_t n, double gamma,
                 uint8_t* d_out, void* stream) {
+  CPB_NVTX_RANGE("cpb_heatmap");
   if (!(gamma > 0.0)) { set_error("gamma must be positive"); return CPB_EINVAL; }
   if (n < 0 || (n > 0 && (!d_p || !d_out))) { set_error("invalid heatmap buffers"); return CPB_EINVAL; }
   return launch_heatmap(d_p, d_valid, n, gamma, d_out, (cudaStream_t)stream);
@@ -493,6 +522,7 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
                         int32_t n_models, const int32_t* kinds, const int32_t* bins,
                         const double* ks, int32_t method, uint64_t seed, int64_t n_samples,
                         uint32_t channels, double* const* h_out, uint8_t* h_valid) {
+  CPB_NVTX_RANGE("cpb_run_host_models");
   if (!h_ens || members < 1 || height < 1 || width < 1) {
     set_error("ensemble needs at least one member and one pixel");
     return CPB_EINVAL;
@@ -790,21 +820,25 @@ int cpb_run_host_models(const float* h_ens, int64_t members, int64_t height, int
 }
 
 int cpb_cases_closed(const cpb_case_batch* batch, double* d_out, void* stream) {
+  CPB_NVTX_RANGE("cpb_cases_closed");
   return launch_cases_closed(batch, d_out, (cudaStream_t)stream);
 }
 
 int cpb_cases_mc(const cpb_case_batch* batch, uint64_t seed, const uint64_t* d_pixels, int64_t n,
                  uint64_t* d_counts, double* d_out, void* stream) {
+  CPB_NVTX_RANGE("cpb_cases_mc");
   return launch_cases_mc(batch, seed, d_pixels, n, (unsigned long long*)d_counts, d_out,
                          (cudaStream_t)stream);
 }
 
 int cpb_cases_semi(const cpb_case_batch* batch, uint64_t seed, const uint64_t* d_pixels, int64_t c,
                    double* d_out, void* stream) {
+  CPB_NVTX_RANGE("cpb_cases_semi");
   return launch_cases_semi(batch, seed, d_pixels, c, d_out, (cudaStream_t)stream);
 }
 
 int cpb_cases_combinatorial(const cpb_case_batch* batch, double* d_out, void* stream) {
+  CPB_NVTX_RANGE("cpb_cases_combinatorial");
   return launch_cases_combinatorial(batch, d_out, (cudaStream_t)stream);
 }
 
@@ -824,6 +858,7 @@ int cpb_run_host(const float* h_ens, int64_t members, int64_t height, int64_t wi
                  int32_t kind, int32_t bins, double k, int32_t method, uint64_t seed,
                  int64_t n_samples, uint32_t channels, double* h_pmin, double* h_pmax,
                  double* h_psaddle, uint8_t* h_valid) {
+  CPB_NVTX_RANGE("cpb_run_host");
   double* outs[3] = {h_pmin, h_pmax, h_psaddle};
   return cpb_run_host_models(h_ens, members, height, width, 1, &kind, &bins, &k, method, seed,
                              n_samples, channels, outs, h_valid);
