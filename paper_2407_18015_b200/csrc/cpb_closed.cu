@@ -482,12 +482,11 @@ CPB_D void uniform_integrals_f32keys(const float* rl, const float* rh, const dou
   uniform_integrals_merged(lo, hi, k, t, acc);
 }
 
-__global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
-    FieldView f, Window w, double* pmin, double* pmax, double* psad, double* partial) {
-  int64_t idx = 0;
-  const bool live = vertex(f, w, idx);
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  if (live) {
+// The four integrals of the uniform vertex idx from the field's planes: with
+// fitted float planes and no degenerate pixel the merge runs on float keys,
+// otherwise load_bounds widens degenerate pixels by eps / 2 (fields.py:140-143).
+CPB_D void uniform_vertex(const FieldView& f, int64_t idx, double acc[4]) {
+  {
     const int64_t at[5] = {idx, idx + 1, idx - f.width, idx - 1, idx + f.width};
     double lo[5], hi[5];
     if (f.bounds == CPB_BOUNDS_F32_FITTED) {
@@ -525,6 +524,16 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
       for (int p = 0; p < 5; ++p) load_bounds(f, at[p], lo[p], hi[p]);
       uniform_integrals(lo, hi, acc);
     }
+  }
+}
+
+__global__ void __launch_bounds__(kClosedThreads) closed_uniform_kernel(
+    FieldView f, Window w, double* pmin, double* pmax, double* psad, double* partial) {
+  int64_t idx = 0;
+  const bool live = vertex(f, w, idx);
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  if (live) {
+    uniform_vertex(f, idx, acc);
     store(pmin, pmax, psad, idx, acc);
   }
   if (partial) warp_partial_sums(acc[0], acc[1], acc[2] + acc[3], partial);
@@ -642,21 +651,28 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
 // Work item = (column band, segment of vertex rows).  A CTA of kFuseCols
 // threads owns the kFuseCols columns [c0, c0 + kFuseCols), c0 a multiple of
 // kFuseCols, and walks its segment's rows top to bottom (one halo row above
-// and below): per row, ONE 2-D TMA box (kFuseBox = kFuseCols + 8 pixels x M
-// members, UTMALDG) starting 4 pixels left of the band -- so the band's own
-// 512 bytes per member row are 128-byte aligned and the two halo columns
-// come from the 16-byte edges the neighbouring bands also read -- lands in a
-// single shared stage; each thread reduces its column's members (FMNMX3.NAN /
-// FMNMX3; threads 0 and 1 also the left / right halo column) into a 4-row ring
-// of (lo, hi), one barrier, the next row's TMA is issued, and vertex row r - 1
-// is stencilled from ring rows r - 2, r - 1, r.  Items come from an atomic
-// work counter (persistent CTAs, dynamic balance).
+// and below): per row, ONE 2-D TMA box (kFuseCols pixels x M members,
+// UTMALDG) of exactly the band's own 512 bytes per member row -- 128-byte
+// aligned, so DRAM moves no byte the band does not use -- lands in a single
+// shared stage; each thread reduces its column's members (FMNMX3.NAN /
+// FMNMX3) into a 4-row ring of (lo, hi), one barrier, the next row's TMA is
+// issued, and vertex row r - 1 is stencilled from ring rows r - 2, r - 1, r.
+// Items come from an atomic work counter (persistent CTAs, dynamic balance).
+// The band's two edge columns need a neighbouring band's fit: the CTA that
+// completes the second of the two bands around a band boundary (a counter per
+// segment and boundary, fenced) then computes that boundary's two columns of
+// the segment from the fitted planes, still hot in L2 (every item also writes
+// its two halo rows, so the segment's own items wrote every pixel those
+// vertices read).  2 of 128 vertices, against the 8
+// extra halo pixels per member row (12.5 % more DRAM sectors) an overlapping
+// box would read.  An edge vertex touching a degenerate pixel is flagged for
+// closed_fuse_edges_kernel (it needs the final eps).
 //
 // The fitted planes are also written (they are the field's params and the
 // input of the finish pass).  A band-row whose stencil touches a degenerate
 // pixel (lo == hi: the eps widening needs the GLOBAL range, unknown until the
 // whole ensemble is read) is not computed here: it is queued in `pending`
-// and computed by closed_fuse_pending_kernel once eps is final.
+// (and flagged) and computed by closed_fuse_pending_kernel once eps is final.
 #ifndef CPB_FUSE_SEG
 #define CPB_FUSE_SEG 128
 #endif
@@ -666,7 +682,7 @@ __global__ void __launch_bounds__(kClosedThreads) closed_uniform_f32_kernel(
 #ifndef CPB_FUSE_EVICT_FIRST  // evict_normal: the halo rows / columns another item re-reads hit L2
 #define CPB_FUSE_EVICT_FIRST 0
 #endif
-constexpr int kFuseCols = 128, kFuseBox = kFuseCols + 8, kFuseRing = kFuseCols + 2;
+constexpr int kFuseCols = 128, kFuseBox = kFuseCols, kFuseRing = kFuseCols + 2;
 constexpr int kFuseSeg = CPB_FUSE_SEG;
 constexpr int kFuseMaxMembers = 256;
 constexpr int kFuseFinishBlocks = 592;
@@ -685,6 +701,10 @@ struct FuseArgs {
   double* psad;
   double* partial;  // (nitems * kFuseCols / 32) warp triples, or null
   int* pending;     // [0] count, then band-rows (row * nbands + band)
+  unsigned char* pflag;  // [(row - row_begin) * nbands + band] = 1: pending band-row (zero at launch)
+  int* bdone;            // [segment][band boundary 0..nbands] adjacent bands done (zero at launch)
+  unsigned char* eflag;  // [edge vertex] = 1: left to the finish pass (degenerate pixel; zero at launch)
+  double* edge_partial;  // (nsegs * (nbands + 1) * kFuseCols / 32) warp triples: in-kernel edge vertices
   int* work;        // work counter, zero at launch
   MultiArgs mf;     // NT >= 0: the planes of every fitted model (multi_fit_pixel)
 };
@@ -709,6 +729,66 @@ CPB_D void fuse_fit_column(const float* col, int M, float& lo, float& hi) {
   }
 }
 
+// Edge vertex e of the range: row (e / per_row), boundary b = (e % per_row) / 2,
+// column b kFuseCols - 1 + (e & 1) -- the two columns on either side of band
+// boundary b (the fused kernel computes columns 1 .. kFuseCols - 2 of a band).
+CPB_D int64_t fuse_edge_col(int64_t k) { return (k >> 1) * kFuseCols - 1 + (k & 1); }
+
+// The two edge columns b kFuseCols - 1, b kFuseCols of row segment [v0, v1)
+// at band boundary b (both bands around it are done): fitted float planes, no
+// eps -- a vertex touching a degenerate pixel is flagged for the finish pass;
+// pending band-rows are skipped (the pending pass redoes them whole).  Fixed
+// thread mapping, one partial triple per warp per (segment, boundary).
+CPB_D void fuse_boundary_edges(const FuseArgs& a, int64_t seg, int64_t b, int64_t v0, int64_t v1) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t per_row = 2 * (int64_t)(a.nbands + 1);
+  const int64_t n = 2 * (v1 - v0);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t e = t; e < n; e += kFuseCols) {
+    const int64_t lr = (v0 - a.row_begin) + (e >> 1), k = 2 * b + (e & 1), c = fuse_edge_col(k);
+    if (c < 1 || c > a.width - 2 || __ldcg(a.pflag + lr * a.nbands + c / kFuseCols)) continue;
+    const int64_t idx = (a.row_begin + lr) * a.width + c;
+    const int64_t at[5] = {idx, idx + 1, idx - a.width, idx - 1, idx + a.width};
+    float rl[5], rh[5];
+    bool deg = false;
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      rl[p] = __ldcg(a.lo + at[p]);  // L2: written by other CTAs of this launch
+      rh[p] = __ldcg(a.hi + at[p]);
+      deg |= !(rh[p] > rl[p]);
+    }
+    if (deg) {
+      a.eflag[lr * per_row + k] = 1;
+      continue;
+    }
+    double lo5[5], hi5[5], acc[4];
+#pragma unroll
+    for (int p = 0; p < 5; ++p) {
+      lo5[p] = (double)rl[p];
+      hi5[p] = (double)rh[p];
+    }
+    uniform_integrals_f32keys(rl, rh, lo5, hi5, acc);
+    store(a.pmin, a.pmax, a.psad, idx, acc);
+    s0 += acc[0];
+    s1 += acc[1];
+    s2 += acc[2] + acc[3];
+  }
+  if (a.edge_partial) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, d);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, d);
+      s2 += __shfl_xor_sync(0xffffffffu, s2, d);
+    }
+    if (lane == 0) {
+      double* q = a.edge_partial + 3 * ((seg * (a.nbands + 1) + b) * (kFuseCols / 32) + warp);
+      q[0] = s0;
+      q[1] = s1;
+      q[2] = s2;
+    }
+  }
+}
+
 // NT < 0: the uniform field alone (min / max per column); NT >= 0: every model
 // of a.mf in the same pass (multi_fit_pixel<NT>: NT histogram bins, 0 = none),
 // the uniform one stencilled.
@@ -721,6 +801,7 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
   float2* ring = reinterpret_cast<float2*>(stage + (size_t)M * kFuseBox);  // [4][kFuseRing]
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + 4 * kFuseRing);
   __shared__ int64_t s_item;
+  __shared__ int s_last2[2];
   if (t == 0) {
     prefetch_tensormap(&map);
     mbar_init(full, 1);
@@ -751,12 +832,9 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
     const int nfit = (int)(v1 - v0) + 2;
     const int64_t c = c0 + t;
     const bool col_ok = c < a.width;
-    // halo column of threads 0 / 1: c0 - 1 (box column 3) / c0 + kFuseCols (box column kFuseCols + 4)
-    const int hbox = t == 0 ? 3 : kFuseCols + 4;
-    const int hring = t == 0 ? 0 : kFuseRing - 1;
     if (t == 0) {
       mbar_arrive_expect_tx(full, box_bytes);
-      tma_load_2d(stage, &map, (int)(f0 * a.width + c0 - 4), 0, full, pol);
+      tma_load_2d(stage, &map, (int)(f0 * a.width + c0), 0, full, pol);
     }
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
     unsigned degmask = 0;  // bit j % 4: ring row j holds a degenerate pixel
@@ -765,21 +843,18 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
       mbar_wait(full, phase);
       phase ^= 1u;
       const bool live = col_ok && r < a.height;
-      const bool own_row = (r >= v0 && r < v1) || (r == 0) || (r == a.height - 1 && r == v1);
+      // every fitted row, the segment's halo rows included (the neighbouring
+      // segment writes the same values): the edge vertices and the finish
+      // passes read them from the planes
+      const bool own_row = true;
       float lo, hi;
       if constexpr (NT < 0)
-        fuse_fit_column(stage + 4 + t, M, lo, hi);
+        fuse_fit_column(stage + t, M, lo, hi);
       else
-        multi_fit_pixel<NT>(stage + 4 + t, kFuseBox, a.mf, r * a.width + c, live && own_row, lo, hi);
+        multi_fit_pixel<NT>(stage + t, kFuseBox, a.mf, r * a.width + c, live && own_row, lo, hi);
       float2* rrow = ring + (j & 3) * kFuseRing;
-      CPB_ASSERT(1 + t < kFuseRing && hbox < kFuseBox && hring < kFuseRing);
+      CPB_ASSERT(1 + t < kFuseRing);
       rrow[1 + t] = make_float2(lo, hi);
-      if (t < 2) {  // the band's halo columns (never degenerate-checked: a halo pixel
-                    // of this band is an own pixel of the next, which checks it)
-        float hl, hh;
-        fuse_fit_column(stage + hbox, M, hl, hh);
-        rrow[hring] = make_float2(hl, hh);
-      }
       if (live) {
         bad |= ((__float_as_uint(lo) & 0x7f800000u) == 0x7f800000u) |
                ((__float_as_uint(hi) & 0x7f800000u) == 0x7f800000u);
@@ -793,26 +868,24 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
       const int rowdeg = __syncthreads_or(live && !(hi > lo));
       if (t == 0 && j + 1 < nfit) {  // every thread is done with the stage
         mbar_arrive_expect_tx(full, box_bytes);
-        tma_load_2d(stage, &map, (int)((r + 1) * a.width + c0 - 4), 0, full, pol);
+        tma_load_2d(stage, &map, (int)((r + 1) * a.width + c0), 0, full, pol);
       }
       degmask = (degmask & ~(1u << (j & 3))) | ((rowdeg ? 1u : 0u) << (j & 3));
       if (j < 2) continue;
       // stencil vertex row r - 1 from ring rows j - 2 (N), j - 1 (C, E, W), j (S)
       const int64_t vr = r - 1;
-      // a degenerate halo pixel is caught by the neighbouring band's own check of
-      // that row, but this band's stencil reads it too: the left / right halo
-      // columns are tested here as well
       const unsigned need = (1u << (j & 3)) | (1u << ((j - 1) & 3)) | (1u << ((j - 2) & 3));
-      const float2 hl = ring[((j - 1) & 3) * kFuseRing], hr = ring[((j - 1) & 3) * kFuseRing + kFuseRing - 1];
-      const bool halo_deg = (c0 > 0 && !(hl.y > hl.x)) || (c0 + kFuseCols < a.width && !(hr.y > hr.x));
-      if ((degmask & need) || halo_deg) {
+      if (degmask & need) {
         if (t == 0) {
           const int q = atomicAdd(a.pending, 1);
           a.pending[1 + q] = (int)(vr * a.nbands + band);
+          a.pflag[(vr - a.row_begin) * a.nbands + band] = 1;
         }
         continue;
       }
-      if (c >= 1 && c <= a.width - 2) {
+      // the band's edge columns t = 0, kFuseCols - 1 need the neighbouring
+      // bands' fits: closed_fuse_edges_kernel computes them
+      if (t >= 1 && t <= kFuseCols - 2 && c <= a.width - 2) {
         const float2* rn = ring + ((j - 2) & 3) * kFuseRing + 1 + t;
         const float2* rc = ring + ((j - 1) & 3) * kFuseRing + 1 + t;
         const float2* rs = ring + (j & 3) * kFuseRing + 1 + t;
@@ -847,6 +920,23 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
         q[2] = s2;
       }
     }
+    // the second band done around a boundary computes that boundary's edge
+    // columns of the segment (boundaries 0 and nbands have one band)
+    __threadfence();  // this item's planes and flags before its counts
+    __syncthreads();
+    if (t < 2) {
+      const int b = band + t;
+      const int need = (b == 0 || b == a.nbands) ? 1 : 2;
+      s_last2[t] = atomicAdd(a.bdone + seg * (a.nbands + 1) + b, 1) == need - 1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      if (s_last2[q]) {
+        __threadfence();  // the other band's planes and flags
+        fuse_boundary_edges(a, seg, band + q, v0, v1);
+      }
+    }
   }
   merge_range(vmin, vmax, bad, a.range);
 }
@@ -878,6 +968,33 @@ __global__ void __launch_bounds__(kFuseCols) closed_fuse_pending_kernel(
     s0 += acc[0];
     s1 += acc[1];
     s2 += acc[2] + acc[3];
+  }
+  if (partial) warp_partial_sums(s0, s1, s2, partial);
+}
+
+// The edge vertices the fused kernel flagged (a degenerate pixel among the
+// five: they need the final eps), in a fixed order: the uniform vertex code of
+// closed_uniform_kernel over the fitted planes (load_bounds widens degenerate
+// pixels by eps / 2).  One edge vertex per thread, one partial triple per warp.
+// pending[0] == -1 (no fused pass ran): every edge vertex of the range.
+__global__ void __launch_bounds__(kFuseCols) closed_fuse_edges_kernel(
+    FieldView f, const int* pending, const unsigned char* pflag, const unsigned char* eflag,
+    int nbands, int64_t row_begin, int64_t row_end, double* pmin, double* pmax, double* psad,
+    double* partial) {
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  const int64_t per_row = 2 * (int64_t)(nbands + 1);
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (pending[0] >= 0 && e < (row_end - row_begin) * per_row && eflag[e]) {
+    const int64_t lr = e / per_row, c = fuse_edge_col(e % per_row);
+    if (!pflag[lr * nbands + c / kFuseCols]) {
+      const int64_t idx = (row_begin + lr) * f.width + c;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      uniform_vertex(f, idx, acc);
+      store(pmin, pmax, psad, idx, acc);
+      s0 = acc[0];
+      s1 = acc[1];
+      s2 = acc[2] + acc[3];
+    }
   }
   if (partial) warp_partial_sums(s0, s1, s2, partial);
 }
@@ -2209,8 +2326,9 @@ int launch_fit(const float* ens, int64_t mstride, cpb_field* f, uint32_t* range,
 namespace {
 struct FuseLayout {
   int nbands;
-  int64_t nsegs, nitems, max_pending;
-  size_t off_pending, off_partial, off_chunk, bytes;
+  int64_t nsegs, nitems, max_pending, n_edges, edge_blocks, nbounds;
+  size_t off_pending, off_flags, off_bdone, off_eflag, off_partial, off_seg_partial, off_chunk, bytes;
+  int64_t ntrip;
 };
 FuseLayout fuse_layout(int64_t width, int64_t row_begin, int64_t row_end) {
   FuseLayout L;
@@ -2219,10 +2337,20 @@ FuseLayout fuse_layout(int64_t width, int64_t row_begin, int64_t row_end) {
   L.nsegs = (rows + kFuseSeg - 1) / kFuseSeg;
   L.nitems = L.nsegs * L.nbands;
   L.max_pending = rows * L.nbands;
+  L.n_edges = rows * 2 * (int64_t)(L.nbands + 1);
+  L.edge_blocks = (L.n_edges + kFuseCols - 1) / kFuseCols;
   L.off_pending = 16;
-  L.off_partial = (L.off_pending + 4 * (size_t)(1 + L.max_pending) + 15) / 16 * 16;
-  const size_t ntrip = (size_t)L.nitems * (kFuseCols / 32) + (size_t)kFuseFinishBlocks * (kFuseCols / 32);
-  L.off_chunk = L.off_partial + ntrip * 3 * sizeof(double);
+  L.off_flags = (L.off_pending + 4 * (size_t)(1 + L.max_pending) + 15) / 16 * 16;
+  L.nbounds = L.nsegs * (L.nbands + 1);
+  L.off_bdone = (L.off_flags + (size_t)L.max_pending + 15) / 16 * 16;
+  L.off_eflag = (L.off_bdone + 4 * (size_t)L.nbounds + 15) / 16 * 16;
+  L.off_partial = (L.off_eflag + (size_t)L.n_edges + 15) / 16 * 16;
+  // warp triples: the fused items, the boundaries' edge vertices, the pending
+  // pass, the flagged-edge pass
+  const int64_t wpb = kFuseCols / 32;
+  L.off_seg_partial = L.off_partial + (size_t)L.nitems * wpb * 3 * sizeof(double);
+  L.ntrip = (L.nitems + L.nbounds + kFuseFinishBlocks + L.edge_blocks) * wpb;
+  L.off_chunk = L.off_partial + (size_t)L.ntrip * 3 * sizeof(double);
   L.bytes = L.off_chunk + (size_t)kCountChunks * 3 * sizeof(double);
   return L;
 }
@@ -2276,10 +2404,12 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* const* fie
     if (rc) return rc;
     cudaError_t e = cudaMemsetAsync(wb + L.off_pending, 0xff, 4, st);  // pending count = -1: all rows
     if (e == cudaSuccess)  // no item partials from the one-pass kernel
-      e = cudaMemsetAsync(wb + L.off_partial, 0, (size_t)L.nitems * (kFuseCols / 32) * 3 * sizeof(double), st);
+      e = cudaMemsetAsync(wb + L.off_partial, 0, (size_t)(L.nitems + L.nbounds) * (kFuseCols / 32) * 3 * sizeof(double), st);
     return e == cudaSuccess ? CPB_OK : cuda_status(e, "memset");
   }
   cudaError_t e = cudaMemsetAsync(wb, 0, L.off_pending + 4, st);  // work counter, pending count
+  // band-row flags, segment counters and edge flags are contiguous
+  if (e == cudaSuccess) e = cudaMemsetAsync(wb + L.off_flags, 0, L.off_partial - L.off_flags, st);
   if (e != cudaSuccess) return cuda_status(e, "memset");
   if (!accumulate) {  // {ordered min = all ones, ordered max = 0, non-finite = 0}
     e = cudaMemsetAsync(range, 0xff, sizeof(uint32_t), st);
@@ -2299,6 +2429,10 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* const* fie
   a.pmin = pmin; a.pmax = pmax; a.psad = psad;
   a.partial = reinterpret_cast<double*>(wb + L.off_partial);
   a.pending = reinterpret_cast<int*>(wb + L.off_pending);
+  a.pflag = reinterpret_cast<unsigned char*>(wb + L.off_flags);
+  a.bdone = reinterpret_cast<int*>(wb + L.off_bdone);
+  a.eflag = reinterpret_cast<unsigned char*>(wb + L.off_eflag);
+  a.edge_partial = reinterpret_cast<double*>(wb + L.off_seg_partial);
   a.work = reinterpret_cast<int*>(wb);
   int nt = -1;
   if (n > 1) {  // the other models' planes come out of the same pass
@@ -2333,7 +2467,7 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* const* fie
   }
   fld->bounds = CPB_BOUNDS_F32_FITTED;
   fld->weights_mode = CPB_WEIGHTS_F64;
-  const size_t smem = (size_t)M * kFuseBox * 4 + 4 * kFuseRing * sizeof(float2) + 16;
+  const size_t smem = (size_t)M * kFuseBox * 4 + 4 * kFuseRing * sizeof(float2) + 16;  // box = the band
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2366,13 +2500,21 @@ int launch_fit_classify_finish(const cpb_field* fld, int64_t row_begin, int64_t 
   const FuseLayout L = fuse_layout(f.width, row_begin, row_end);
   char* wb = static_cast<char*>(work);
   double* partial = reinterpret_cast<double*>(wb + L.off_partial);
+  const int* pending = reinterpret_cast<const int*>(wb + L.off_pending);
+  const int64_t wpb = kFuseCols / 32;
+  double* part_pending = partial + 3 * (size_t)(L.nitems + L.nbounds) * wpb;
   closed_fuse_pending_kernel<<<kFuseFinishBlocks, kFuseCols, 0, st>>>(
-      f, reinterpret_cast<const int*>(wb + L.off_pending), L.nbands, row_begin, row_end, pmin, pmax, psad,
-      partial + 3 * (size_t)L.nitems * (kFuseCols / 32));
+      f, pending, L.nbands, row_begin, row_end, pmin, pmax, psad, part_pending);
   CPB_CHECK_LAUNCH("fused stencil: pending rows");
+  if (L.edge_blocks > 0)
+    closed_fuse_edges_kernel<<<(unsigned)L.edge_blocks, kFuseCols, 0, st>>>(
+        f, pending, reinterpret_cast<const unsigned char*>(wb + L.off_flags),
+        reinterpret_cast<const unsigned char*>(wb + L.off_eflag), L.nbands, row_begin, row_end, pmin, pmax,
+        psad, part_pending + 3 * (size_t)kFuseFinishBlocks * wpb);
+  CPB_CHECK_LAUNCH("fused stencil: flagged band edges");
   if (counts) {
     double* chunk = reinterpret_cast<double*>(wb + L.off_chunk);
-    const int64_t n = L.nitems * (kFuseCols / 32) + (int64_t)kFuseFinishBlocks * (kFuseCols / 32);
+    const int64_t n = L.ntrip;
     counts_reduce_kernel<<<kCountChunks, 256, 0, st>>>(partial, n, chunk);
     counts_finish_kernel<<<1, 256, 0, st>>>(chunk, kCountChunks, counts);
     CPB_CHECK_LAUNCH("fused stencil: counts");
