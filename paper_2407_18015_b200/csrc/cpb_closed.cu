@@ -842,16 +842,15 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
       const int64_t r = f0 + j;
       mbar_wait(full, phase);
       phase ^= 1u;
+      // every fitted row is written to the planes, the segment's halo rows
+      // included (the neighbouring segment writes the same values): the edge
+      // vertices and the finish passes read them there
       const bool live = col_ok && r < a.height;
-      // every fitted row, the segment's halo rows included (the neighbouring
-      // segment writes the same values): the edge vertices and the finish
-      // passes read them from the planes
-      const bool own_row = true;
       float lo, hi;
       if constexpr (NT < 0)
         fuse_fit_column(stage + t, M, lo, hi);
       else
-        multi_fit_pixel<NT>(stage + t, kFuseBox, a.mf, r * a.width + c, live && own_row, lo, hi);
+        multi_fit_pixel<NT>(stage + t, kFuseBox, a.mf, r * a.width + c, live, lo, hi);
       float2* rrow = ring + (j & 3) * kFuseRing;
       CPB_ASSERT(1 + t < kFuseRing);
       rrow[1 + t] = make_float2(lo, hi);
@@ -860,7 +859,7 @@ __global__ void __launch_bounds__(kFuseCols, CPB_FUSE_MINB) closed_fuse_uniform_
                ((__float_as_uint(hi) & 0x7f800000u) == 0x7f800000u);
         vmin = fminf(vmin, lo);
         vmax = fmaxf(vmax, hi);
-        if (NT < 0 && own_row) {
+        if (NT < 0) {
           a.lo[r * a.width + c] = lo;
           a.hi[r * a.width + c] = hi;
         }
