@@ -10,7 +10,8 @@ for m in uniform epanechnikov histogram; do
 done
 STEPS=20 timeout 900 bash tools/bench_config3.sh
 timeout 1500 bash tools/prof_full.sh
-for b in 8 16 32; do
+# (gpurun copies back <= 64 MiB: SKIP_C3_NCU=1 leaves out the three config-3 reports)
+[ -n "$SKIP_C3_NCU" ] || for b in 8 16 32; do
   P="python bench.py --height 2048 --width 2048 --members 40 --bins $b --models histogram --fit separate --no-e2e --no-cpu --steps 1 --warmup 1 --profile"
   $P > gpurun_out/prof_c3_plain.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:"closed_hist" -c 1 -o gpurun_out/prof_c3_b${b}_${TAG} $P > gpurun_out/prof_c3_ncu_b$b.log 2>&1; tail -1 gpurun_out/prof_c3_ncu_b$b.log
 done
