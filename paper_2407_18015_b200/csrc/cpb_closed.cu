@@ -1195,18 +1195,18 @@ CPB_D void epan_piece_n(double a, double b, const double* m, const double* ih, u
 // deterministic.
 constexpr int kPPWarps = 4;
 
-// closed_pp_kernel's per-warp layout: ROWS rows of vertex constants (uniform
-// lo, hi, inv; Epanechnikov m, ih, plus the MX float copies), the piece ends,
-// and per slot the (owner lane, neighbour states) word in the r2 slot.  Slot e
-// is read and written only by lane e % 32, so its results overwrite its own
+// closed_pp_kernel's per-warp layout: ROWS rows of vertex constants
+// (Epanechnikov m, ih, plus the MX float copies), the piece ends, and per slot
+// the (owner lane, neighbour states, degree class) word in the r2 slot.  Slot
+// e is read and written only by lane e % 32, so its results overwrite its own
 // (a, b, owner) words, and the vertex's fast-mode flag is the sign of its
-// centre ih (inv) row.  Epanechnikov fp64: 9.25 KB per warp, six 4-warp blocks
-// per SM (24 warps).
+// centre ih row.  Epanechnikov fp64: 9.25 KB per warp, six 4-warp blocks per
+// SM (24 warps).
 template <int ROWS>
 struct PPSmem {
   double vd[ROWS][32];
   double pa[9 * 32], pb[9 * 32];  // piece ends, then results min / max
-  double r2[9 * 32];              // owner | state << 8, then result saddle (t1 + t2)
+  double r2[9 * 32];              // owner | state << 8 | class << 16, then result saddle (t1 + t2)
 };
 
 // Mixed-precision Epanechnikov piece (CPB_FLAG_MIXED): positions re-centred on
