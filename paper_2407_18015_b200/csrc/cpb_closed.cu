@@ -2395,8 +2395,12 @@ int launch_fit_classify(const float* ens, int64_t mstride, cpb_field* const* fie
   }
   const FuseLayout L = fuse_layout(W, row_begin, row_end);
   char* wb = static_cast<char*>(work);
-  if (M < 1 || M > kFuseMaxMembers || mstride % 4 != 0 || (reinterpret_cast<uintptr_t>(ens) & 15) ||
-      H * W >= ((int64_t)1 << 31) || (slot[1] && slot[1]->bins > kThreshBinsPix)) {
+  // per-row TMA boxes start at pixel r W + c0: their global address is
+  // 16-byte aligned only when W is a multiple of 4 (a misaligned box start
+  // faults as an illegal instruction)
+  if (M < 1 || M > kFuseMaxMembers || mstride % 4 != 0 || W % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(ens) & 15) || H * W >= ((int64_t)1 << 31) ||
+      (slot[1] && slot[1]->bins > kThreshBinsPix)) {
     // not one TMA-streamed pass: the plain fit(s) now, every vertex row in the finish pass
     int rc = n == 1 ? launch_fit(ens, mstride, fld, range, accumulate, st)
                     : launch_fit_multi(ens, mstride, fields, n, range, accumulate, st);

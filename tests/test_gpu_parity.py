@@ -729,6 +729,46 @@ def test_fused_fit_classify_uniform_bitexact(shape):
     assert max(np.max(np.abs(out[c] - oref[ch])) for c, ch in enumerate(("min", "max", "saddle"))) <= CLOSED_TOL
 
 
+def test_fused_fit_classify_band_edges_and_degenerate_edges():
+    """The fused kernel reads only its own 128-column band and computes the band
+    edge columns (127 / 128, 255 / 256, ...) in-kernel once both bands around a
+    boundary are done; an edge vertex touching a degenerate pixel is flagged and
+    redone with the final eps by the finish pass.  Degenerate pixels right at
+    the band boundaries and at a row-segment boundary (row 128), bit-exact
+    against fit + classify and within tolerance of the oracle."""
+    M, H, W = 9, 300, 392  # W % 4 == 0 and H W % 4 == 0: the TMA-streamed path
+    vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=11)
+    for r, c in ((40, 127), (41, 128), (90, 255), (90, 256), (128, 200), (129, 128), (200, 383), (250, 1)):
+        vals[:, r, c] = vals[0, r, c]  # lo == hi: widened by the global eps at use
+    dev, out, counts, _ = _fused_uniform(vals)
+    ref = cpb.classify_field(_fit(vals, "uniform"))
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(out[c], ref.channel(ch)), (ch, np.max(np.abs(out[c] - ref.channel(ch))))
+        assert abs(counts[c] - ref.channel(ch).sum()) <= 1e-9 * max(1.0, abs(counts[c]))
+    oref = orc.classify(orc.fit(vals, "uniform"), "uniform")
+    assert max(np.max(np.abs(out[c] - oref[ch])) for c, ch in enumerate(("min", "max", "saddle"))) <= CLOSED_TOL
+    # partial row range starting inside a segment, band edges included (no
+    # degenerate pixels here: a partial range sees only its rows' eps)
+    plain = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=11)
+    dev, out, counts, _ = _fused_uniform(plain, 100, 260)
+    pref = cpb.classify_field(_fit(plain, "uniform"))
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(out[c][100:260], pref.channel(ch)[100:260]), ch
+
+
+@pytest.mark.parametrize("shape", [(9, 200, 390), (9, 200, 391), (5, 40, 130)])
+def test_fused_fit_classify_unaligned_rows(shape):
+    """Widths that are not a multiple of 4 with a 16-byte member stride: the
+    per-row TMA box would start misaligned (an illegal-instruction fault), so
+    the fused call takes the plain fit + finish path -- same results."""
+    M, H, W = shape
+    vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=W)
+    dev, out, counts, _ = _fused_uniform(vals)
+    ref = cpb.classify_field(_fit(vals, "uniform"))
+    for c, ch in enumerate(("min", "max", "saddle")):
+        assert np.array_equal(out[c], ref.channel(ch)), ch
+
+
 def test_fused_fit_classify_partial_rows_and_nonfinite():
     M, H, W = 12, 50, 140
     vals = orc.ackley_ensemble(W, H, M, noise_amp=0.3, seed=1)
