@@ -252,6 +252,12 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # CPB_BENCH_BACKEND=gloo + CPB_BENCH_SHARE_GPU=1: a dry run of the N-rank
+    # flow on one GPU (ranks share it, collectives staged through host copies);
+    # the measured run is NCCL with one GPU per rank
+    backend = os.environ.get("CPB_BENCH_BACKEND", "nccl")
+    if os.environ.get("CPB_BENCH_SHARE_GPU") == "1":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
@@ -259,8 +265,11 @@ def run_ours(args):
         # the transport (NVLink / NVLS) NCCL chose; stdout keeps the one JSON line
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=device)
-        print(f"[bench] rank {rank}/{world}: NCCL process group on cuda:{local} "
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
+        print(f"[bench] rank {rank}/{world}: {backend} process group on cuda:{local} "
               f"({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
     H, W, M, bins = args.height, args.width, args.members, args.bins
     models = [m for m in args.models.split(",") if m]
@@ -399,7 +408,7 @@ def run_ours(args):
     ms = t0.elapsed_time(t1)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        D._all_reduce(t, dist.ReduceOp.MAX)
         ms = float(t[0])
     per_kernel = timer.collect()
     ms_step = ms / args.steps
@@ -737,7 +746,7 @@ def run_e2e(args, models, slab, rank, world, device):
         one()
     dist.barrier()
     sec = torch.tensor([(time.perf_counter() - t) / steps], dtype=torch.float64, device=device)
-    dist.all_reduce(sec, op=dist.ReduceOp.MAX)
+    D._all_reduce(sec, dist.ReduceOp.MAX)
     return {"value": round(nm * verts / float(sec[0]) / 1e6, 2), "unit": "Mvertices/s",
             "h2d_bytes_per_step": M * H * W * 4,
             "d2h_bytes_per_step": nm * 3 * H * W * 8, "steps": steps,
@@ -830,7 +839,7 @@ def relaunch(args):
     import torch
 
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and os.environ.get("CPB_BENCH_SHARE_GPU") != "1":
         sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}")
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

@@ -116,3 +116,23 @@ def test_slab_ranks_as_processes_match_single_gpu(world):
                 # every rank holds the SUM all-reduced expected counts
                 want = [ref_c.channel(ch).sum() for ch in ("min", "max", "saddle")]
                 assert np.allclose(sums, want, rtol=1e-12, atol=1e-9), (kind, sums, want)
+
+
+def test_bench_multirank_dry_run(tmp_path):
+    """bench.py --gpus 2 end to end (self-launch under torch.distributed.run,
+    per-rank slabs, max-over-ranks timing, rank-0 parity bands, the N > 1 e2e
+    pipeline) with the test-only gloo / shared-GPU switches; the measured run
+    is the same flow over NCCL with one GPU per rank."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CPB_BENCH_BACKEND="gloo", CPB_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--height", "1026",
+                        "--width", "1024", "--members", "8", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, env=env, cwd=root, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["parity"]["ok"], line["parity"]
