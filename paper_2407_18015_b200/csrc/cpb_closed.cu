@@ -362,8 +362,8 @@ CPB_D void merge_pairs8_tagged(double* k, int* t) {
 // moves that neighbour below -> inside -> above.  A 2-bit crossing count per
 // neighbour replaces the per-piece midpoint comparisons (8 FP64-pipe compares
 // per piece), and the 9 pieces are unrolled so the keys are static registers.
-// Ties are harmless: coincident points bound zero-width pieces, which are
-// skipped, and a count of 2 means "above" whatever the tie order.
+// Ties are harmless: coincident points bound zero-width pieces, which add
+// exactly 0, and a count of 2 means "above" whatever the tie order.
 template <bool FAST>
 CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const double* inv,
                                  const double* k, const int* t, double acc[4]) {
@@ -373,7 +373,10 @@ CPB_D void uniform_pieces_tagged(const double* lo, const double* hi, const doubl
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
     const double b = i < 8 ? k[i] : hi[C_];
-    if (b > a) {
+    // every piece is evaluated (a zero-width one adds s * 0 = exactly 0): no
+    // per-piece branch, so the nine unrolled pieces schedule as one block
+    // (fused uniform kernel 15.5 -> 15.0 ms)
+    {
       const double half = 0.5 * (b - a), mid = 0.5 * (b + a);
       double al[5], be[5];
 #pragma unroll
