@@ -233,9 +233,13 @@ class KernelTimer:
         else:
             self.pending.append((self.kind, what, self.open, ev))
 
-    def collect(self):
+    def collect(self, origin=None):
         self.torch.cuda.synchronize()
         out = {}
+        if origin is not None and os.environ.get("CPB_BENCH_TIMELINE") == "1":  # diagnostic
+            for kind, what, a, b in self.pending:
+                print(f"[bench] timeline {kind}/{what}: {origin.elapsed_time(a):9.3f} .. "
+                      f"{origin.elapsed_time(b):9.3f} ms", file=sys.stderr)
         for kind, what, a, b in self.pending:
             out.setdefault((kind, what), []).append(a.elapsed_time(b))
         self.pending = []
@@ -288,8 +292,9 @@ def run_ours(args):
         _lib.check(_lib.load().cpb_set_option(b"fit_ctas_per_sm", args.fit_ctas))
     # the fits (HBM / issue bound) on a high-priority stream run under the
     # previous stencils (FP64 bound) on a low-priority one
-    s_fit = torch.cuda.Stream(device=device, priority=-1)
-    s_cls = torch.cuda.Stream(device=device, priority=0)
+    fit_pri = int(os.environ.get("CPB_BENCH_FIT_PRIORITY", "-1"))  # diagnostic: -1 high, 0 low
+    s_fit = torch.cuda.Stream(device=device, priority=fit_pri)
+    s_cls = torch.cuda.Stream(device=device, priority=-1 - fit_pri)
     fused = args.fit in ("fused", "fused-stencil") and len(models) > 1
     # the uniform stencil runs inside the fit pass (cpb_fit_multi_classify): a
     # uniform-only step is ONE kernel; with several models the pass also writes
@@ -398,9 +403,14 @@ def run_ours(args):
     t1 = torch.cuda.Event(enable_timing=True)
     wall0 = time.time()
     t0.record()
+    host_ms = []
     for _ in range(args.steps):
+        h0 = time.perf_counter()
         step()
+        host_ms.append((time.perf_counter() - h0) * 1e3)
     t1.record()
+    if os.environ.get("CPB_BENCH_HOSTTIME") == "1":  # host enqueue time per step (diagnostic)
+        print(f"[bench] host ms per step: {[round(x, 2) for x in host_ms]}", file=sys.stderr)
     torch.cuda.synchronize()
     clocks.mark(wall0, time.time())
     barrier()
@@ -410,7 +420,7 @@ def run_ours(args):
         t = torch.tensor([ms], dtype=torch.float64, device=device)
         D._all_reduce(t, dist.ReduceOp.MAX)
         ms = float(t[0])
-    per_kernel = timer.collect()
+    per_kernel = timer.collect(origin=t0)
     ms_step = ms / args.steps
     verts = (H - 2) * (W - 2)
     value = len(models) * verts / (ms_step / 1e3) / 1e6
