@@ -1,4 +1,4 @@
+# histogram advance-test variants: parity with the integer-key build, then A/B
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_f.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_f.log
-timeout 600 python tools/run_reference_tests.py > gpurun_out/reftests_f.log 2>&1; echo "reftests rc=$?"; tail -1 gpurun_out/reftests_f.log | cut -c1-300
-timeout 300 python tools/bench_estimators.py > gpurun_out/est_f.log 2>&1; cat gpurun_out/est_f.log
+timeout 600 python -m pytest tests -m gpu -x -q -k "hist or shapes or closed or golden" > gpurun_out/pytest_f.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_f.log
+VARIANTS="adv0 adv1 adv2" CMD="python bench.py --models histogram --no-e2e --no-cpu --steps 5 --warmup 3" REPS=3 timeout 900 bash tools/ab.sh
