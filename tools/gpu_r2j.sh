@@ -1,6 +1,4 @@
+# histogram tile 16 x 16 (324 staged pixels per 256 vertices) vs 32 x 8 (340): parity, then A/B
 mkdir -p gpurun_out
-VARIANTS="base ada2" CMD="python bench.py --models epanechnikov --no-e2e --steps 5 --warmup 3" REPS=2 timeout 900 bash tools/ab.sh
-grep -o '"max_abs_err": {[^}]*}' gpurun_out/ab_ada2.log | head -2
-P="python bench.py --models epanechnikov --height 8192 --width 8192 --members 64 --no-e2e --no-cpu --steps 1 --warmup 1 --profile"
-cp ab/ada2.so paper_2407_18015_b200/libcritprob_b200.so
-$P > gpurun_out/prof_pp_plain_ada2.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:closed_pp -c 1 -o gpurun_out/prof_pp_ada2 $P > gpurun_out/prof_pp_ncu_ada2.log 2>&1; tail -1 gpurun_out/prof_pp_ncu_ada2.log
+timeout 600 python -m pytest tests -m gpu -x -q -k "hist or shapes or closed or golden or slab" > gpurun_out/pytest_j.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_j.log
+VARIANTS="t32 t16" CMD="python bench.py --models histogram --no-e2e --no-cpu --steps 5 --warmup 3" REPS=3 timeout 900 bash tools/ab.sh
