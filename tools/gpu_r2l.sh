@@ -1,3 +1,4 @@
+# histogram sweep advancing only the tournament's arg-min list (ties -> zero-width pieces): parity, then A/B
 mkdir -p gpurun_out
-VARIANTS="ada3 ada4" CMD="python bench.py --models epanechnikov --no-e2e --steps 5 --warmup 3" REPS=2 timeout 900 bash tools/ab.sh
-grep -o '"max_abs_err": {[^}]*}' gpurun_out/ab_ada4.log | head -2
+timeout 600 python -m pytest tests -m gpu -x -q -k "hist or shapes or closed or golden or slab" > gpurun_out/pytest_l.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_l.log
+VARIANTS="am0 am2" CMD="python bench.py --models histogram --no-e2e --no-cpu --steps 5 --warmup 3" REPS=3 timeout 900 bash tools/ab.sh
